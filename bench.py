@@ -1,0 +1,330 @@
+"""Strait estimator + dispatch on B200 — benchmark driver.
+
+Headline workload (BASELINE.json configs[2], "candidate-sweep microbench"):
+one scheduling ROUND = the candidate sweep over 2^24 (candidate, GPU,
+co-runner) triples (2^22 pairs x 4 slots, 2^16 segments x 64 GPU states)
+fused with the sequential online refit of F = 64 feedback samples, in one
+launch (strait_round).  Metric: latency predictions/sec (one per projected
+co-runner triple + one check_meet estimate per pair).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1: launched by torchrun, one rank per GPU; every rank sweeps its own
+round of the same shape (weak scaling, no data-path collective); the only
+collective is the end-of-run NCCL all-reduce of the timing / checksum.
+--impl reference times the CPU oracle port of the reference path
+(oracle/, all host threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "latency predictions/sec (candidate sweep + refit round)"
+UNIT = "predictions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--segments", type=int, default=1 << 16)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def predictions_per_round(soa) -> int:
+    return soa.n_triples + soa.n_pairs
+
+
+def config_block(args, ws):
+    return {"workload": "C3 candidate-sweep microbench (BASELINE configs[2])",
+            "segments_per_gpu": args.segments, "gpus_per_segment": 64, "slots": 4,
+            "triples_per_gpu_round": args.segments * 64 * 4, "refit_samples_per_round": 64,
+            "n_metrics": 5, "parallelism": f"replicated rounds x{ws} (weak)",
+            "l2": "inputs (2.5 GB/round) > 126 MB L2; no flush needed"}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+            "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+            "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.reasons |= {k for k, b in names.items() if r & b and k != "gpu_idle"}
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.nv:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def cpu_round_rate(soa, fb, seconds: float, threads: int):
+    """Oracle port: full sweep rounds (+ refit) on `threads` host threads for ~`seconds`."""
+    from oracle import oracle
+
+    P = np.array([0.1, np.e, 0.0] + [0.1] * 5 + [0.1, 0.1, 0.5, 1.0])
+    state = np.concatenate([P, np.zeros(24)])
+    t0 = time.perf_counter()
+    rounds = 0
+    segs = 0
+    chunk = max(256, soa.n_segments // 8)
+    while True:
+        for s0 in range(0, soa.n_segments, chunk):
+            oracle.sweep(soa, state[:12], threads=threads, seg_range=(s0, min(soa.n_segments, s0 + chunk)))
+            segs += min(soa.n_segments, s0 + chunk) - s0
+            if time.perf_counter() - t0 > seconds:
+                break
+        else:
+            state, _, _, _, _ = oracle.refit(state, rounds, fb, nm=5)
+            rounds += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    preds = segs * 64 * 4 + segs * 64
+    return preds / dt, dt, segs
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2604_28175_b200.microbench import c3_feedback, c3_round
+
+    soa = c3_round(0, n_segments=args.segments)
+    fb = c3_feedback(0)
+    threads = os.cpu_count() or 1
+    t_budget = max(5.0, min(120.0, args.cpu_seconds))
+    per_step = []
+    for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
+        rate, dt, segs = cpu_round_rate(soa, fb, t_budget / 3, threads)
+        per_step.append(rate)
+    value = float(np.median(per_step))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(per_step),
+        "warmup": 0, "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "impl": "reference", "config": config_block(args, ws),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"oracle/strait_oracle.c sweep+refit over the C3 round, ~{t_budget / 3:.0f}s "
+                                   f"per step on {threads} threads (OpenMP)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_28175_b200 import _abi
+    from paper_2604_28175_b200 import _device as D
+    from paper_2604_28175_b200 import sweep as SW
+    from paper_2604_28175_b200.microbench import algorithmic_bytes, c3_feedback, c3_round
+    from paper_2604_28175_b200.predictor import InterferencePredictor
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _abi.lib()
+
+    soa_h = c3_round(rank, n_segments=args.segments)
+    n_rounds = args.warmup + args.steps
+    fbs = [c3_feedback(rank * 100000 + r) for r in range(max(n_rounds, args.e2e_steps + 1))]
+    soa = soa_h.to_device()
+    pred = InterferencePredictor()
+    P0 = torch.tensor(pred.params.to_vector(), dtype=torch.float64, device="cuda")
+    stateA = torch.tensor(pred.params.to_vector() + pred.opt.m + pred.opt.v, dtype=torch.float64, device="cuda")
+    stateB = stateA.clone()
+    step = torch.zeros(1, dtype=torch.int64, device="cuda")
+    from paper_2604_28175_b200.predictor import bias_correction_tables
+
+    b1, b2 = bias_correction_tables(pred.opt.beta1, pred.opt.beta2, n_rounds * 64 + 64)
+    bc = (D.dev(b1), D.dev(b2))
+    dfb = [{k: D.dev(v, torch.int8 if k == "prio" else torch.float64) for k, v in f.items()} for f in fbs]
+    out = SW.alloc_outputs(soa)
+    stream = torch.cuda.current_stream()
+    np_ = pred.params.n_params()
+
+    def one_round(r, cur, nxt, events=None):
+        # params of round r = cur[:np]; the refit writes round r+1's state into nxt
+        nxt.copy_(cur)
+        f = dfb[r % len(dfb)]
+        args_r, _ = pred.refit_args(nxt, step, 64, f["twa"], f["self_cmp"], f["self_mem"], f["prio"],
+                                    f["actual"], bc=bc)
+        if events:
+            events[0].record()
+        SW.launch_round(soa, cur[:np_], out, args_r)
+        if events:
+            events[1].record()
+
+    cur, nxt = stateA, stateB
+    for r in range(args.warmup):
+        one_round(r, cur, nxt)
+        cur, nxt = nxt, cur
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.strait_kernel_launches()
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        t_start.record()
+        for i in range(args.steps):
+            one_round(args.warmup + i, cur, nxt, kev[i])
+            cur, nxt = nxt, cur
+        t_end.record()
+        torch.cuda.synchronize()
+    launches = lib.strait_kernel_launches() - launches0
+    elapsed_ms = t_start.elapsed_time(t_end)
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    path = SW.last_sweep_path()
+
+    # end to end through the public API: pinned host SoA -> H2D -> round -> D2H decisions
+    pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in soa_h.arrays.items()}
+    h2d = sum(t.numel() * t.element_size() for t in pinned.values())
+    host_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in out.items()}
+    d2h = sum(t.numel() * t.element_size() for t in host_out.values())
+    e2e_ms = []
+    for i in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for k, t in pinned.items():
+            soa.arrays[k].copy_(t, non_blocking=True)
+        one_round(i, cur, nxt)
+        cur, nxt = nxt, cur
+        for k, t in out.items():
+            host_out[k].copy_(t, non_blocking=True)
+        ev1.record()
+        torch.cuda.synchronize()
+        if i:  # first iteration warms the pinned copies
+            e2e_ms.append(ev0.elapsed_time(ev1))
+    e2e_step_ms = float(np.mean(e2e_ms))
+
+    preds = predictions_per_round(soa_h)
+    alg_bytes = algorithmic_bytes(soa_h)
+    checksum = float(np.nansum(host_out["seg_latency"].numpy())) + float(host_out["seg_gpu"].numpy().sum())
+    vec = torch.tensor([elapsed_ms, e2e_step_ms, kern_ms, checksum], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        mx = vec.clone()
+        dist.all_reduce(mx[:3], op=dist.ReduceOp.MAX)
+        sm = vec.clone()
+        dist.all_reduce(sm[3:], op=dist.ReduceOp.SUM)
+        vec = torch.cat([mx[:3], sm[3:]])
+    elapsed_ms, e2e_step_ms, kern_ms_max, checksum = (float(x) for x in vec.tolist())
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    ms_per_step = elapsed_ms / args.steps
+    value = ws * preds * args.steps / (elapsed_ms / 1e3)
+    peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    if os.path.exists(peaks_path):
+        peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    tfile = os.path.join(REPO, "profiles", "sweep_traffic.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "impl": "ours",
+        "config": config_block(args, ws),
+        "triples_per_s": ws * soa_h.n_triples * args.steps / (elapsed_ms / 1e3),
+        "e2e": {"value": ws * preds / (e2e_step_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step_ms,
+                "path": "pinned host SoA -> H2D -> strait_round (C-ABI) -> D2H decisions"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_src, "kernel": f"strait_round ({path} sweep path)",
+                     "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": kern_ms},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+        "checksum": checksum,
+    }
+    if not args.no_cpu_baseline:
+        from paper_2604_28175_b200.microbench import c3_feedback as _fb
+
+        threads = os.cpu_count() or 1
+        rate, dt, segs = cpu_round_rate(soa_h, _fb(0), args.cpu_seconds, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                                "sample": f"oracle sweep+refit, {segs} segments of the C3 round in {dt:.1f}s"}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

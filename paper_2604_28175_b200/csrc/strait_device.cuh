@@ -1,0 +1,97 @@
+// strait_device.cuh — binary64 device arithmetic of the Strait estimator.
+//
+// Every helper restates one reference function (file:line under
+// /root/reference/pkg/src/infersim) in its exact left-to-right evaluation
+// order.  The library is compiled with --fmad=false -prec-div=true
+// -prec-sqrt=true so that each `a * b + c` below rounds twice, like CPython.
+// The only deviations from the reference are libdevice exp/log/pow (<= 1-2 ulp
+// from glibc on a small fraction of inputs), which the parity tests bound.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/strait.h"
+
+namespace strait {
+
+constexpr double kLogSaturate = 500.0;  // predictor.py:27 _LOG_SATURATE
+constexpr int kMaxM = STRAIT_MAX_METRICS;
+constexpr int kMaxP = STRAIT_MAX_METRICS + 7;
+
+// CPython builtin max(a, b) / min(a, b): first-wins, NaN-propagating.
+__host__ __device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
+__host__ __device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
+
+// Parameters of one predictor, staged in registers/shared memory by callers.
+template <int NM>
+struct Pred {
+  double scale, offset, log_base;  // log_base = math.log(params.base), hoisted (same value per call)
+  double w[NM];
+  double w_cmp, w_mem;
+  double coeff[2];  // [HIGH, LOW]
+  double cap;
+
+  __device__ __forceinline__ void load(const double* __restrict__ P, double effect_cap) {
+    scale = P[0];
+    log_base = log(P[1]);
+    offset = P[2];
+#pragma unroll
+    for (int i = 0; i < NM; ++i) w[i] = P[3 + i];
+    w_cmp = P[3 + NM];
+    w_mem = P[4 + NM];
+    coeff[0] = P[5 + NM];
+    coeff[1] = P[6 + NM];
+    cap = effect_cap;
+  }
+
+  // predictor.py:161-176 pressure_exponent — self terms first, then metrics.
+  __device__ __forceinline__ double exponent(const double (&a)[NM], double cmp, double mem) const {
+    double x = w_cmp * cmp + w_mem * mem;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) x += w[i] * a[i];
+    return x;
+  }
+
+  // predictor.py:179-195 _raw_effect + kernel_effect.
+  __device__ __forceinline__ double effect(double x, bool& saturated) const {
+    const double z = x * log_base;
+    if (z > kLogSaturate) {
+      saturated = true;
+      return cap;
+    }
+    const double inner = scale * exp(z) + offset;
+    saturated = inner >= cap;
+    if (saturated) return cap;
+    return py_min(py_max(inner, 0.0), cap);
+  }
+
+  // predictor.py:198-216 interference_degree(kernel_effect(pressure_exponent(...))).
+  __device__ __forceinline__ double predict(const double (&a)[NM], double cmp, double mem, int prio,
+                                            bool& saturated) const {
+    const double x = exponent(a, cmp, mem);
+    const double eff = effect(x, saturated);
+    return 1.0 + eff * (prio == 0 ? coeff[0] : coeff[1]);
+  }
+  __device__ __forceinline__ double predict(const double (&a)[NM], double cmp, double mem,
+                                            int prio) const {
+    bool s;
+    return predict(a, cmp, mem, prio, s);
+  }
+};
+
+// Runtime-NM dispatch: instantiate `F<NM>` for NM = 1..8.
+#define STRAIT_DISPATCH_NM(nm, F, ...)                 \
+  switch (nm) {                                        \
+    case 1: F<1>(__VA_ARGS__); break;                  \
+    case 2: F<2>(__VA_ARGS__); break;                  \
+    case 3: F<3>(__VA_ARGS__); break;                  \
+    case 4: F<4>(__VA_ARGS__); break;                  \
+    case 5: F<5>(__VA_ARGS__); break;                  \
+    case 6: F<6>(__VA_ARGS__); break;                  \
+    case 7: F<7>(__VA_ARGS__); break;                  \
+    case 8: F<8>(__VA_ARGS__); break;                  \
+    default: break;                                    \
+  }
+
+}  // namespace strait

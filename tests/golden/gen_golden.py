@@ -1,0 +1,278 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE
+(`infersim`, imported read-only from /root/reference/pkg/src) on seeded
+inputs.  The fixtures pin the CPU oracle (oracle/) and the CUDA path.
+
+    python tests/golden/gen_golden.py            # all fixtures
+    python tests/golden/gen_golden.py replay     # only the replay fixtures
+
+Run in the build container (the reference does not exist on the GPU box;
+the committed .npz files travel instead).
+"""
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+sys.path.insert(0, REPO)
+
+from infersim.domain import Batch, PriorityLevel, Request, ThroughputTimeline  # noqa: E402
+from infersim.predictor import (FeedbackSample, InterferencePredictor, PredictorParams, kernel_effect,  # noqa: E402
+                                predict_interference, pressure_exponent)
+from infersim.profiles import random_profile  # noqa: E402
+from infersim.runtime import GpuRuntimeState, RunningTaskEntry  # noqa: E402
+from infersim.scheduler import check_meet, check_violate  # noqa: E402
+
+
+def params_vec(p: PredictorParams):
+    return np.asarray(p.to_vector(), dtype=np.float64)
+
+
+def random_params(rng, nm=5):
+    return PredictorParams(
+        scale=float(rng.uniform(0.01, 2.0)), base=float(rng.uniform(1.1, 4.0)),
+        offset=float(rng.uniform(-1.0, 1.0)), weights=tuple(float(w) for w in rng.uniform(-0.5, 0.8, nm)),
+        self_compute_weight=float(rng.uniform(-0.5, 0.8)), self_memory_weight=float(rng.uniform(-0.5, 0.8)),
+        priority_coeff={PriorityLevel.HIGH: float(rng.uniform(0.1, 1.0)),
+                        PriorityLevel.LOW: float(rng.uniform(0.5, 2.0))},
+    )
+
+
+def gen_predict():
+    """c01-style draws (test_acceptance.py:96-138): 100 parameter sets x 100
+    inputs, plus saturation / clamp edge cases."""
+    rng = np.random.default_rng(1)
+    P, A, CM, ME, PR, X, EFF, INTF, SAT = [], [], [], [], [], [], [], [], []
+    for _ in range(100):
+        p = random_params(rng)
+        for j in range(100):
+            scale_in = 2.5 if j < 90 else 400.0  # a few far-out inputs saturate (z > 500 / inner >= cap)
+            a = tuple(float(v) for v in rng.uniform(0.0, scale_in, 5))
+            c, m = float(rng.uniform(0, 1)), float(rng.uniform(0, 1))
+            pr = PriorityLevel(int(rng.integers(0, 2)))
+            x = pressure_exponent(p, a, c, m)
+            from infersim.predictor import _raw_effect
+            _, sat = _raw_effect(p, x)
+            P.append(params_vec(p)); A.append(a); CM.append(c); ME.append(m); PR.append(int(pr))
+            X.append(x); EFF.append(kernel_effect(p, x)); INTF.append(predict_interference(p, a, c, m, pr))
+            SAT.append(sat)
+    np.savez_compressed(os.path.join(HERE, "predict.npz"), params=np.array(P), coloc=np.array(A),
+                        self_cmp=np.array(CM), self_mem=np.array(ME), prio=np.array(PR, np.int8),
+                        exponent=np.array(X), effect=np.array(EFF), intf=np.array(INTF), saturated=np.array(SAT))
+
+
+def gen_latency():
+    from infersim.pcie import PcieLinkState
+    from infersim.predictor import estimate_latency
+    from infersim.profiles import default_profiles
+    rng = np.random.default_rng(11)
+    profiles = list(default_profiles().values())
+    rows = {k: [] for k in ("params", "assumed", "cmp", "mem", "prio", "total", "kernel", "t_avail", "front",
+                            "now", "latency")}
+    for _ in range(2000):
+        p = random_params(rng)
+        prof = profiles[int(rng.integers(0, len(profiles)))]
+        k = int(rng.integers(1, 9))
+        now = float(rng.uniform(0, 1000))
+        link = PcieLinkState(t_available=now + float(rng.uniform(-5, 5)))
+        front = now - float(rng.uniform(0, 10))
+        assumed = tuple(float(v) for v in rng.uniform(0, 1.5, 5))
+        lat = estimate_latency(p, prof, k, front, link, now, assumed)
+        for key, val in (("params", params_vec(p)), ("assumed", assumed), ("cmp", prof.self_compute_at(k)),
+                         ("mem", prof.self_memory_at(k)), ("prio", int(prof.priority)),
+                         ("total", prof.total_latency_ms(k)), ("kernel", prof.kernel_latency_ms(k)),
+                         ("t_avail", link.t_available), ("front", front), ("now", now), ("latency", lat)):
+            rows[key].append(val)
+    np.savez_compressed(os.path.join(HERE, "latency.npz"), **{k: np.array(v) for k, v in rows.items()})
+
+
+def gen_refit():
+    """Three sequential update streams through InterferencePredictor.update:
+    c07-style noisy convergence, adversarial floors (test_predictor.py:392-410)
+    and a stream with saturating / non-finite samples."""
+    out = {}
+    hidden = PredictorParams(scale=0.35, base=2.3, offset=-0.15, weights=(0.22, 0.28, 0.18, 0.25, 0.2),
+                             self_compute_weight=0.3, self_memory_weight=0.15,
+                             priority_coeff={PriorityLevel.HIGH: 0.6, PriorityLevel.LOW: 1.0})
+    for name, seed, n in (("converge", 7, 3000), ("adversarial", 5, 2000), ("edge", 9, 400)):
+        rng = np.random.default_rng(seed)
+        pred = InterferencePredictor()
+        tw, cm, me, pr, ac = [], [], [], [], []
+        res_p, res_r, res_s, res_sat, traj = [], [], [], [], []
+        for i in range(n):
+            if name == "converge":
+                agg = tuple(float(a) for a in rng.uniform(0.0, 2.0, 5))
+                c, m = float(rng.uniform(0.1, 0.9)), float(rng.uniform(0.1, 0.9))
+                p = PriorityLevel.HIGH if rng.uniform() < 0.4 else PriorityLevel.LOW
+                truth = predict_interference(hidden, agg, c, m, p)
+                actual = 1.0 + (truth - 1.0) * math.exp(float(rng.normal(0.0, 0.05)))
+            elif name == "adversarial":
+                agg = tuple(float(a) for a in rng.uniform(0, 2, 5))
+                c, m = float(rng.uniform(0, 1)), float(rng.uniform(0, 1))
+                p = PriorityLevel(int(rng.integers(0, 2)))
+                actual = float(rng.uniform(0.2, 6.0))
+            else:
+                big = i % 7 == 3
+                agg = tuple(float(a) for a in rng.uniform(0, 60.0 if big else 2.0, 5))
+                c, m = float(rng.uniform(0, 1)), float(rng.uniform(0, 1))
+                p = PriorityLevel(int(rng.integers(0, 2)))
+                actual = math.inf if i % 11 == 5 else float(rng.uniform(0.5, 8.0))
+            r = pred.update(FeedbackSample("b", agg, c, m, p, actual))
+            tw.append(agg); cm.append(c); me.append(m); pr.append(int(p)); ac.append(actual)
+            res_p.append(r.predicted); res_r.append(r.residual); res_s.append(r.skipped); res_sat.append(r.saturated)
+            traj.append(pred.params.to_vector() + pred.opt.m + pred.opt.v + [pred.opt.step])
+        out.update({f"{name}_twa": np.array(tw).T.copy(), f"{name}_cmp": np.array(cm), f"{name}_mem": np.array(me),
+                    f"{name}_prio": np.array(pr, np.int8), f"{name}_actual": np.array(ac),
+                    f"{name}_predicted": np.array(res_p), f"{name}_residual": np.array(res_r),
+                    f"{name}_skipped": np.array(res_s), f"{name}_saturated": np.array(res_sat),
+                    f"{name}_traj": np.array(traj)})
+    init = InterferencePredictor()
+    out["init_state"] = np.array(init.params.to_vector() + init.opt.m + init.opt.v)
+    np.savez_compressed(os.path.join(HERE, "refit.npz"), **out)
+
+
+def rebuild_pair(soa, p, profiles_by_idx):
+    """Reference GpuRuntimeState for pair p of the SoA (object-level rebuild)."""
+    nm, Cs = soa.n_metrics, soa.n_slots
+    g = p % soa.gpus_per_segment
+    gpu = GpuRuntimeState(g, nm, soa.concurrency_limit)
+    nrun = int(soa.arrays["gpu_n_running"][p])
+    Tn = soa.n_triples
+    for c in range(nrun):
+        t = p * Cs + c
+        prio = PriorityLevel(int(soa.arrays["ent_prio"][t]))
+        req = Request(f"r{t}", "m", soa.now - 50.0, soa.now + 1000.0)
+        batch = Batch(f"b{t}", "m", 1, prio, req.arrival_time, [req])
+        twa = tuple(float(soa.arrays["ent_twa"][m, t]) for m in range(nm))
+        e = RunningTaskEntry(
+            batch=batch,
+            contribution=tuple(float(soa.arrays["ent_contrib"][m, t]) for m in range(nm)),
+            self_compute=float(soa.arrays["ent_self_cmp"][t]), self_memory=float(soa.arrays["ent_self_mem"][t]),
+            kernel_latency_ms=float(soa.arrays["ent_t_kernel"][t]),
+            deadline_abs=float(soa.arrays["ent_deadline_abs"][t]), intf_predicted=1.0,
+            kernel_start_estimate=float(soa.arrays["ent_kstart"][t]),
+            timeline=ThroughputTimeline([(soa.now, twa)]),  # TWA(now) == twa exactly (total <= 0 branch)
+        )
+        gpu.running.append(e)
+    gpu._recompute_aggregate()
+    agg = np.array(gpu.aggregate_throughput)
+    assert np.array_equal(agg, soa.arrays["gpu_agg"][:, p]), "generator aggregate != reference list-order sum"
+    assert np.array_equal(np.array(gpu.low_priority_aggregate()), soa.arrays["gpu_lp_agg"][:, p])
+    gpu.aimd.cap_pct = float(soa.arrays["gpu_cap_pct"][p])
+    gpu.pcie.t_available = float(soa.arrays["gpu_t_avail"][p])
+    del Tn
+    return gpu
+
+
+def reference_sweep(soa, pred, ref_profiles, use_violate=True, use_meet=True):
+    """best_for (scheduler.py:263-280) on rebuilt objects for every segment."""
+    S, G = soa.n_segments, soa.gpus_per_segment
+    flags = np.zeros(S * G, np.uint8)
+    plat = np.full(S * G, np.nan)
+    pintf = np.full(S * G, np.nan)
+    sg = np.full(S, -1, np.int32)
+    sl = np.full(S, np.nan)
+    si = np.full(S, np.nan)
+    for s in range(S):
+        prof = ref_profiles[int(soa.meta["cand_model"][s])]
+        k = int(soa.meta["cand_size"][s])
+        front = float(soa.arrays["cand_front"][s])
+        best = None
+        for g in range(G):
+            p = s * G + g
+            gpu = rebuild_pair(soa, p, ref_profiles)
+            if not gpu.has_slot():
+                continue
+            f = 1
+            v = check_violate(gpu, prof, k, soa.now, pred)
+            ok, lat, intf, _ = check_meet(gpu, prof, k, front, soa.now, pred)
+            f |= (2 if v else 0) | (4 if ok else 0)
+            admitted = not (use_violate and v) and not (use_meet and not ok)
+            if admitted:
+                f |= 8
+                if best is None or (lat, g) < (best[0], best[1]):
+                    best = (lat, g, intf)
+            flags[p], plat[p], pintf[p] = f, lat, intf
+        if best is not None:
+            sl[s], sg[s], si[s] = best
+    return dict(pair_flags=flags, pair_latency=plat, pair_intf=pintf, seg_gpu=sg, seg_latency=sl, seg_intf=si)
+
+
+def gen_sweep():
+    from paper_2604_28175_b200.microbench import c3_round
+    rng = np.random.default_rng(2604)
+    ref_profiles = [random_profile(rng, f"m{i:02d}", PriorityLevel.HIGH if i < 8 else PriorityLevel.LOW)
+                    for i in range(32)]
+    from paper_2604_28175_b200.profiles import profile_to_dict
+    from infersim.profiles import profile_to_dict as ref_to_dict
+    from paper_2604_28175_b200.microbench import c3_profiles
+    assert [profile_to_dict(p) for p in c3_profiles()] == [ref_to_dict(p) for p in ref_profiles]
+    cases = {
+        "c3": dict(round_idx=0, n_segments=48, gpus=64, slots=4),
+        "small": dict(round_idx=1, n_segments=300, gpus=4, slots=4),
+        "odd": dict(round_idx=2, n_segments=111, gpus=3, slots=4),
+    }
+    preds = {
+        "default": InterferencePredictor(),
+        "strong": InterferencePredictor(PredictorParams(scale=0.5, base=2.6, offset=-0.4,
+                                                        weights=(0.3, 0.25, 0.35, 0.2, 0.3),
+                                                        self_compute_weight=0.25, self_memory_weight=0.2)),
+    }
+    out = {}
+    for cname, kw in cases.items():
+        soa = c3_round(profiles=None, **kw)
+        for k, v in soa.arrays.items():
+            out[f"{cname}__in__{k}"] = v
+        for k, v in soa.meta.items():
+            out[f"{cname}__meta__{k}"] = v
+        out[f"{cname}__geom"] = np.array([soa.n_metrics, soa.n_slots, soa.gpus_per_segment, soa.concurrency_limit,
+                                          soa.n_segments])
+        for pname, pred in preds.items():
+            out[f"{cname}__{pname}__params"] = params_vec(pred.params)
+            variants = [("full", True, True)] + ([("no_meet", True, False), ("no_violate", False, True)]
+                                                 if cname == "small" else [])
+            for vname, uv, um in variants:
+                res = reference_sweep(soa, pred, ref_profiles, uv, um)
+                for k, v in res.items():
+                    out[f"{cname}__{pname}__{vname}__{k}"] = v
+    np.savez_compressed(os.path.join(HERE, "sweep.npz"), **out)
+
+
+def gen_twa():
+    """Random step-hold timelines -> reference time_weighted_average."""
+    rng = np.random.default_rng(21)
+    rows = {k: [] for k in ("t0", "t_last", "v_last", "acc", "end", "twa", "ns")}
+    from paper_2604_28175_b200.domain import ThroughputTimeline as MyTL
+    for i in range(3000):
+        n = int(rng.integers(1, 9))
+        t = 100.0 * rng.uniform()
+        ref, mine = ThroughputTimeline(), MyTL()
+        for j in range(n):
+            if j and rng.uniform() < 0.2:
+                pass  # same timestamp -> replace
+            else:
+                t += float(rng.exponential(1.0))
+            v = tuple(float(x) for x in rng.uniform(0, 2, 5))
+            ref.record(t, v)
+            mine.record(t, v)
+        end = t + (0.0 if i % 5 == 0 else float(rng.exponential(2.0)))
+        twa = ref.time_weighted_average(end)
+        rows["t0"].append(mine.times[0]); rows["t_last"].append(mine.times[-1])
+        rows["v_last"].append(mine.values[-1]); rows["acc"].append(mine.acc); rows["end"].append(end)
+        rows["twa"].append(twa); rows["ns"].append(len(ref))
+    np.savez_compressed(os.path.join(HERE, "twa.npz"),
+                        **{k: (np.array(v).T.copy() if k in ("v_last", "acc", "twa") else np.array(v))
+                           for k, v in rows.items()})
+
+
+if __name__ == "__main__":
+    what = sys.argv[1:] or ["predict", "latency", "refit", "sweep", "twa"]
+    for w in what:
+        print("generating", w, flush=True)
+        globals()[f"gen_{w}"]()

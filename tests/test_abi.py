@@ -1,0 +1,43 @@
+"""CPU: the C-ABI library loads and exports every symbol include/*.h declares
+(no compute calls — there is no GPU here)."""
+import ctypes
+import glob
+import os
+import re
+
+from conftest import REPO
+
+
+def declared_symbols():
+    names = set()
+    for h in glob.glob(os.path.join(REPO, "include", "*.h")):
+        text = open(h).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        names |= set(re.findall(r"\b(strait_\w+)\s*\(", text))
+    return names
+
+
+def test_header_declares_entry_points():
+    names = declared_symbols()
+    for must in ("strait_predict", "strait_estimate_latency", "strait_sweep", "strait_refit", "strait_round",
+                 "strait_twa", "strait_abi_version", "strait_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2604_28175_b200 import _abi
+
+    lib = _abi.lib()
+    missing = [n for n in sorted(declared_symbols()) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert lib.strait_abi_version() == 1
+    assert isinstance(lib.strait_last_error(), bytes)
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    from paper_2604_28175_b200 import _abi
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _abi.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
