@@ -12,10 +12,13 @@
 //               (scheduler.py:130-135), check_meet (:164-185) on the leader lane
 //   3. segment: best_for's lexicographic (latency, gpu_id) argmin over the
 //               segment's pairs (:263-280), one warp per segment over shared memory.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "strait_capi.cuh"
 #include "strait_device.cuh"
@@ -54,11 +57,11 @@ struct StageLayout {
   __host__ __device__ StageLayout(const TileGeom& t) {
     ent = 0;
     eprio = ent + (size_t)kEntF * t.TT * 8;
-    pair = align_up(eprio + t.TT, 16);
+    pair = align_up(eprio + t.TT, 128);  // TMA tensor-copy destination
     nrun = pair + (size_t)kPairF * t.TP * 8;
     cand = align_up(nrun + t.TP, 16);
     cprio = cand + (size_t)kCandF * t.spb * 8;
-    bytes = align_up(cprio + t.spb, 128);
+    bytes = align_up(cprio + 4 * t.spb, 128);  // TMA path stores the aligned 4-byte word holding each prio
     tx_bytes = (size_t)kEntF * t.TT * 8 + t.TT + (size_t)kPairF * t.TP * 8 + t.TP;
   }
 };
@@ -326,128 +329,292 @@ __global__ void __launch_bounds__(kSweepThreads + 32, 2)
   tile_compute<NM, C>(a, tg, L, CL, smem, smem, seg0, e);
 }
 
-// ============================================================== TMA pipeline kernel
-// Persistent CTAs walk tiles blockIdx.x, +gridDim.x, ...  Thread 0 keeps
-// `nstages` tiles in flight: every triple/pair field chunk of a tile is one
-// cp.async.bulk into the stage's shared memory, completing on the stage's
-// mbarrier (expect_tx = the tile's byte count).  Candidate values (one 8-byte
-// value per field) ride one tile ahead in registers of the first threads.
+// ============================================================== warp-specialized TMA pipeline
+// Persistent CTAs walk the tiles blockIdx.x, +gridDim.x, ...  Roles:
+//   * producer warp: for every tile waits the stage's EMPTY barrier, posts the
+//     tile's byte count on its FULL barrier and issues one cp.async.bulk per
+//     SoA field chunk (one lane per chunk); candidate values (8 bytes per
+//     field, below the bulk-copy granule) ride one tile ahead in registers and
+//     are stored into the stage before the producer arrives on FULL.
+//   * `groups` x 8 consumer warps: group q takes every groups-th tile; a warp
+//     owns 32 consecutive triples of the tile.  No CTA-wide barriers: each warp
+//     computes its triples, ORs pairs with shuffles, writes pair results into
+//     the stage, and the LAST warp of the tile to finish (shared atomic
+//     counter) runs best_for's argmin for the tile's segments.  Each warp then
+//     releases the stage (EMPTY arrive, 8 per tile).
+//   * optional refit warp (CTA 0 only): the serial Adam chain of strait_round.
+// One bulk copy of a tile: src = src0 + tile * stride, into stage + dst.
+struct BulkCopy {
+  const char* src0;
+  int64_t stride;
+  uint32_t dst, bytes;
+};
+
+template <int NM>
+struct WsLayout {
+  StageLayout<NM> st;
+  size_t res_lat, res_intf, res_adm, cnt, stage_bytes;
+  size_t pred, full, empty, refit, copies, bytes;
+  __host__ __device__ WsLayout(const TileGeom& t, int nstages) : st(t) {
+    res_lat = st.bytes;
+    res_intf = res_lat + (size_t)t.TP * 8;
+    res_adm = res_intf + (size_t)t.TP * 8;
+    cnt = align_up(res_adm + t.TP, 16);
+    stage_bytes = align_up(cnt + 16, 128);
+    pred = stage_bytes * nstages;
+    full = align_up(pred + sizeof(Pred<NM>), 16);
+    empty = full + 8 * kMaxStages;
+    refit = empty + 8 * kMaxStages;
+    copies = align_up(refit + 8 * kMaxP, 16);
+    bytes = copies + sizeof(BulkCopy) * (4 * kMaxM + 9);
+  }
+};
+
+constexpr int kWsMaxStages = kMaxStages;
+
+template <int NM>
+__device__ __forceinline__ int n_bulk_copies() { return (2 * NM + 5) + 1 + (2 * NM + 2) + 1; }
+
+// Table of the tile's bulk copies (built once per CTA): every SoA field chunk
+// of a tile is contiguous, so copy i of tile t is src0_i + t * stride_i.
 template <int NM, int C>
-__device__ __forceinline__ void issue_tile_tma(const StraitSweepArgs& a, const TileGeom& tg,
-                                               const StageLayout<NM>& L, unsigned char* stage, uint64_t* bar,
-                                               int64_t tile, uint64_t pol) {
+__device__ __forceinline__ int build_copy_table(const StraitSweepArgs& a, const TileGeom& tg, const StageLayout<NM>& L,
+                                                BulkCopy* tab) {
   const int64_t S = a.n_segments, Pn = S * tg.G, Tn = Pn * C;
-  const int64_t t0 = tile * tg.TT, p0 = tile * tg.TP;
   const uint32_t tb = tg.TT * 8, pb = tg.TP * 8;
-  mbar_arrive_expect_tx(bar, (uint32_t)L.tx_bytes);
-  double* ent = (double*)(stage + L.ent);
-#pragma unroll
-  for (int m = 0; m < NM; ++m) {
-    bulk_g2s(ent + m * tg.TT, a.ent_contrib + m * Tn + t0, tb, bar, pol);
-    bulk_g2s(ent + (NM + m) * tg.TT, a.ent_twa + m * Tn + t0, tb, bar, pol);
-  }
-  bulk_g2s(ent + (2 * NM + 0) * tg.TT, a.ent_self_cmp + t0, tb, bar, pol);
-  bulk_g2s(ent + (2 * NM + 1) * tg.TT, a.ent_self_mem + t0, tb, bar, pol);
-  bulk_g2s(ent + (2 * NM + 2) * tg.TT, a.ent_t_kernel + t0, tb, bar, pol);
-  bulk_g2s(ent + (2 * NM + 3) * tg.TT, a.ent_deadline_abs + t0, tb, bar, pol);
-  bulk_g2s(ent + (2 * NM + 4) * tg.TT, a.ent_kstart + t0, tb, bar, pol);
-  bulk_g2s(stage + L.eprio, a.ent_prio + t0, tg.TT, bar, pol);
-  double* pair = (double*)(stage + L.pair);
-#pragma unroll
-  for (int m = 0; m < NM; ++m) {
-    bulk_g2s(pair + m * tg.TP, a.gpu_agg + m * Pn + p0, pb, bar, pol);
-    bulk_g2s(pair + (NM + m) * tg.TP, a.gpu_lp_agg + m * Pn + p0, pb, bar, pol);
-  }
-  bulk_g2s(pair + (2 * NM) * tg.TP, a.gpu_cap_pct + p0, pb, bar, pol);
-  bulk_g2s(pair + (2 * NM + 1) * tg.TP, a.gpu_t_avail + p0, pb, bar, pol);
-  bulk_g2s(stage + L.nrun, a.gpu_n_running + p0, tg.TP, bar, pol);
+  int n = 0;
+  auto add = [&](const void* base, int64_t stride, size_t dst, uint32_t bytes) {
+    tab[n++] = BulkCopy{(const char*)base, stride, (uint32_t)dst, bytes};
+  };
+  for (int m = 0; m < NM; ++m) add(a.ent_contrib + m * Tn, tb, L.ent + (size_t)m * tb, tb);
+  for (int m = 0; m < NM; ++m) add(a.ent_twa + m * Tn, tb, L.ent + (size_t)(NM + m) * tb, tb);
+  const double* ef[5] = {a.ent_self_cmp, a.ent_self_mem, a.ent_t_kernel, a.ent_deadline_abs, a.ent_kstart};
+  for (int j = 0; j < 5; ++j) add(ef[j], tb, L.ent + (size_t)(2 * NM + j) * tb, tb);
+  add(a.ent_prio, tg.TT, L.eprio, tg.TT);
+  for (int m = 0; m < NM; ++m) add(a.gpu_agg + m * Pn, pb, L.pair + (size_t)m * pb, pb);
+  for (int m = 0; m < NM; ++m) add(a.gpu_lp_agg + m * Pn, pb, L.pair + (size_t)(NM + m) * pb, pb);
+  add(a.gpu_cap_pct, pb, L.pair + (size_t)(2 * NM) * pb, pb);
+  add(a.gpu_t_avail, pb, L.pair + (size_t)(2 * NM + 1) * pb, pb);
+  add(a.gpu_n_running, tg.TP, L.nrun, tg.TP);
+  return n;
 }
 
-template <int NM, int C>
-__global__ void __launch_bounds__(kSweepThreads + 32, 1)
-    sweep_tma_kernel(const StraitSweepArgs a, const StraitRefitArgs r, int with_refit, int nstages) {
+// SG != 0 fixes gpus_per_segment at compile time (SG * C == 256: one segment per
+// tile) so every shared-memory offset folds into an immediate.
+template <int NM, int C, int SG>
+__global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
+    sweep_ws_kernel(const StraitSweepArgs a, const StraitRefitArgs r, int with_refit, int nstages, int groups,
+                    int diag, const __grid_constant__ CUtensorMap ent_map,
+                    const __grid_constant__ CUtensorMap pair_map, int use_tmap) {
   extern __shared__ __align__(128) unsigned char smem[];
-  const TileGeom tg(a.gpus_per_segment, C);
-  const StageLayout<NM> L(tg);
-  const CtaLayout<NM> CL(tg, L, nstages);
-  if (threadIdx.x >= kSweepThreads) {
-    if (with_refit && blockIdx.x == 0) refit_warp<NM>(r, (double*)(smem + CL.refit));
-    return;
-  }
-  const int tid = threadIdx.x;
+  const TileGeom tg(SG ? SG : a.gpus_per_segment, C);
+  const WsLayout<NM> W(tg, nstages);
+  const StageLayout<NM>& L = W.st;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_cons = 8 * groups;
   const int64_t ntiles = a.n_segments / tg.spb;
-  uint64_t* bars = (uint64_t*)(smem + CL.bars);
-  const uint64_t pol = l2_evict_first_policy();
-  constexpr int kCF = StageLayout<NM>::kCandF;
-  if (tid == 0) {
-    ((Pred<NM>*)(smem + CL.pred))->load(a.params, a.effect_cap);
-    for (int st = 0; st < nstages; ++st) mbar_init(&bars[st], 1);
+  uint64_t* full = (uint64_t*)(smem + W.full);
+  uint64_t* empty = (uint64_t*)(smem + W.empty);
+  const int ncand = tg.spb * StageLayout<NM>::kCandF;
+
+  BulkCopy* ctab = (BulkCopy*)(smem + W.copies);
+  if (threadIdx.x == 0) {
+    ((Pred<NM>*)(smem + W.pred))->load(a.params, a.effect_cap);
+    build_copy_table<NM, C>(a, tg, L, ctab);
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(&full[s], 32);  // the producer warp's cp.async arrivals; bulk bytes via expect_tx
+      mbar_init(&empty[s], 8);
+      *(int*)(smem + s * W.stage_bytes + W.cnt) = 0;
+    }
     fence_mbar_init();
   }
-  group_sync(kSweepThreads);
-  // prologue: fill the pipeline; candidate values of the first tile
-  int64_t tile = blockIdx.x;
-  if (tid == 0)
-    for (int st = 0; st < nstages; ++st) {
-      const int64_t tt = tile + (int64_t)st * gridDim.x;
-      if (tt < ntiles) issue_tile_tma<NM, C>(a, tg, L, smem + st * L.bytes, &bars[st], tt, pol);
-    }
-  const int ncand = tg.spb * kCF;
-  if (tile < ntiles && tid < ncand + tg.spb) {
-    unsigned char* stage = smem;  // stage 0
-    if (tid < ncand) {
-      const int f = tid / tg.spb, sl = tid - f * tg.spb;
-      ((double*)(stage + L.cand))[tid] = cand_field<NM>(a, f, tile * tg.spb + sl);
-    } else {
-      ((int8_t*)(stage + L.cprio))[tid - ncand] = __ldg(a.cand_prio + tile * tg.spb + (tid - ncand));
-    }
-  }
-  group_sync(kSweepThreads);
+  __syncthreads();
 
-  for (int64_t k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+  if (warp == n_cons + 1) {  // ---------------------------------------------- refit warp
+    if (with_refit && blockIdx.x == 0) refit_warp<NM>(r, (double*)(smem + W.refit));
+    return;
+  }
+  if (warp == n_cons) {  // ------------------------------------------------- producer warp
+    const uint64_t pol = l2_evict_first_policy();
+    if (use_tmap && lane == 0) {
+      prefetch_tmap(&ent_map);
+      prefetch_tmap(&pair_map);
+    }
+    int64_t tile = blockIdx.x;
+    for (int64_t k = 0; tile < ntiles; ++k, tile += gridDim.x) {
+      const int st = (int)(k % nstages);
+      const uint32_t use = (uint32_t)(k / nstages);
+      unsigned char* stage = smem + st * W.stage_bytes;
+      mbar_wait(&empty[st], (use & 1) ^ 1);
+      if (lane == 0 && use_tmap) {
+        // packed SoA: two 2-D boxes ([2NM+5] x TT triple fields, [2NM+2] x TP pair fields) + 2 byte arrays
+        mbar_expect_tx(&full[st], (uint32_t)L.tx_bytes);
+        tma_2d_g2s(stage + L.ent, &ent_map, (int)(tile * tg.TT), 0, &full[st], pol);
+        tma_2d_g2s(stage + L.pair, &pair_map, (int)(tile * tg.TP), 0, &full[st], pol);
+        const BulkCopy& e = ctab[2 * NM + 5];
+        bulk_g2s(stage + e.dst, e.src0 + tile * e.stride, e.bytes, &full[st], pol);
+        const BulkCopy& n = ctab[n_bulk_copies<NM>() - 1];
+        bulk_g2s(stage + n.dst, n.src0 + tile * n.stride, n.bytes, &full[st], pol);
+      } else if (lane == 0) {
+        mbar_expect_tx(&full[st], (uint32_t)L.tx_bytes);
+        for (int i = 0; i < n_bulk_copies<NM>(); ++i) {
+          const BulkCopy cp = ctab[i];
+          if (diag & 1) bulk_g2s_nohint(stage + cp.dst, cp.src0 + tile * cp.stride, cp.bytes, &full[st]);
+          else bulk_g2s(stage + cp.dst, cp.src0 + tile * cp.stride, cp.bytes, &full[st], pol);
+        }
+      }
+      // candidate values (8 B per field and segment) and the aligned words holding the priorities
+      for (int i = lane; i < ncand + tg.spb; i += 32) {
+        if (i < ncand) {
+          const int f = i / tg.spb, sl = i - f * tg.spb;
+          const int64_t s = tile * tg.spb + sl;
+          const double* src = f < NM ? a.cand_contrib + f * a.n_segments + s
+                            : f == NM ? a.cand_self_cmp + s : f == NM + 1 ? a.cand_self_mem + s
+                            : f == NM + 2 ? a.cand_total + s : f == NM + 3 ? a.cand_kernel + s
+                            : f == NM + 4 ? a.cand_front + s : a.cand_deadline + s;
+          cp_async_8((double*)(stage + L.cand) + i, src);
+        } else {
+          const int64_t s = tile * tg.spb + (i - ncand);
+          cp_async_4((uint32_t*)(stage + L.cprio) + (i - ncand), a.cand_prio + (s & ~int64_t(3)));
+        }
+      }
+      cp_async_mbar_arrive_noinc(&full[st]);  // one of the 32 expected arrivals per phase
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------------ consumer warps
+  const int group = warp >> 3, wg = warp & 7;
+  const int local = wg * 32 + lane;  // triple within the tile
+  const bool active = local < tg.TT;
+  const int sl = active ? local / tg.span : 0;
+  const int rr = local - sl * tg.span;
+  const int g = rr / C;
+  const int c = rr - g * C;
+  const int pl = sl * tg.G + g;
+  const int TP = tg.TP, TT = tg.TT, spb = tg.spb, G = tg.G;
+  const double now = a.now;
+  const Pred<NM>& pr = *(const Pred<NM>*)(smem + W.pred);
+  const double nan = __longlong_as_double(0x7ff8000000000000LL);
+
+  int64_t tile = blockIdx.x + (int64_t)group * gridDim.x;
+  for (int64_t k = group; tile < ntiles; k += groups, tile += (int64_t)groups * gridDim.x) {
     const int st = (int)(k % nstages);
-    unsigned char* stage = smem + st * L.bytes;
-    const int64_t next = tile + gridDim.x;
-    // candidate values of the next tile: issued now, stored after compute
-    double cnext = 0.0;
-    int8_t pnext = 0;
-    const bool cand_thread = next < ntiles && tid < ncand + tg.spb;
-    if (cand_thread) {
-      if (tid < ncand) {
-        const int f = tid / tg.spb, sl = tid - f * tg.spb;
-        cnext = cand_field<NM>(a, f, next * tg.spb + sl);
-      } else {
-        pnext = __ldg(a.cand_prio + next * tg.spb + (tid - ncand));
-      }
+    const uint32_t use = (uint32_t)(k / nstages);
+    unsigned char* stage = smem + st * W.stage_bytes;
+    mbar_wait(&full[st], use & 1);
+    if (diag & 2) {  // diagnostic: data movement only
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      continue;
     }
-    mbar_wait(&bars[st], (uint32_t)((k / nstages) & 1));
-    TripleRegs<NM> e;
-    {
-      const double* ent = (const double*)(stage + L.ent);
+
+    const double* ent = (const double*)(stage + L.ent);
+    const double* pair = (const double*)(stage + L.pair);
+    const double* cand = (const double*)(stage + L.cand);
+    double* s_lat = (double*)(stage + W.res_lat);
+    double* s_intf = (double*)(stage + W.res_intf);
+    uint8_t* s_adm = (uint8_t*)(stage + W.res_adm);
+
+    // ---- 1. triple projection (scheduler.py:137-160) ----
+    const int nrun = active ? ((const int8_t*)(stage + L.nrun))[pl] : 0;
+    const int cprio = active ? ((const int8_t*)(stage + L.cprio))[4 * sl + (int)((tile * spb + sl) & 3)] : 0;
+    const int eprio = active ? ((const int8_t*)(stage + L.eprio))[local] : 0;
+    bool viol = false;
+    if (active && c < nrun && eprio <= cprio) {
+      double tw[NM], nagg[NM];
 #pragma unroll
-      for (int m = 0; m < NM; ++m) {
-        e.ec[m] = ent[m * tg.TT + tid];
-        e.tw[m] = ent[(NM + m) * tg.TT + tid];
+      for (int m = 0; m < NM; ++m) tw[m] = ent[(NM + m) * TT + local];
+      const double cmp = ent[(2 * NM + 0) * TT + local], mem = ent[(2 * NM + 1) * TT + local];
+      const double tk = ent[(2 * NM + 2) * TT + local], ks = ent[(2 * NM + 4) * TT + local];
+      const double intf_cur = pr.predict(tw, cmp, mem, eprio);
+      const double elapsed = py_max(0.0, now - ks);
+      const double denom = intf_cur * tk;
+      const double progress = denom > 0 ? py_min(1.0, elapsed / denom) : 1.0;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) nagg[m] = pair[m * TP + pl] - ent[m * TT + local] + cand[m * spb + sl];
+      const double intf_new = pr.predict(nagg, cmp, mem, eprio);
+      const double remaining = (1.0 - progress) * tk * intf_new;
+      const double projected = py_max(now, ks) + remaining;
+      viol = projected > ent[(2 * NM + 3) * TT + local];
+    }
+    unsigned vbits = viol ? 1u : 0u;
+#pragma unroll
+    for (int o = C / 2; o > 0; o >>= 1) vbits |= __shfl_xor_sync(0xffffffffu, vbits, o, C);
+
+    // ---- 2. pair: LP cap + check_meet on the leader lane ----
+    if (active && c == 0) {
+      uint8_t flags = 0;
+      double lat = nan, intf = nan;
+      bool admitted = false;
+      if (nrun < a.concurrency_limit) {
+        flags |= STRAIT_PAIR_HAS_SLOT;
+        bool violate = vbits != 0;
+        if (cprio == 1) {
+          const double cap_fraction = pair[(2 * NM) * TP + pl] / 100.0;
+#pragma unroll
+          for (int m = 0; m < NM; ++m)
+            if (pair[(NM + m) * TP + pl] + cand[m * spb + sl] > cap_fraction) violate = true;
+        }
+        if (violate) flags |= STRAIT_PAIR_VIOLATE;
+        double assumed[NM];
+#pragma unroll
+        for (int m = 0; m < NM; ++m) assumed[m] = 0.5 * pair[m * TP + pl];
+        intf = pr.predict(assumed, cand[(NM + 0) * spb + sl], cand[(NM + 1) * spb + sl], cprio);
+        const double wait = py_max(0.0, pair[(2 * NM + 1) * TP + pl] - now);
+        lat = cand[(NM + 2) * spb + sl] + wait + (intf - 1.0) * cand[(NM + 3) * spb + sl] +
+              (now - cand[(NM + 4) * spb + sl]);
+        const bool ok = lat <= cand[(NM + 5) * spb + sl];
+        if (ok) flags |= STRAIT_PAIR_MEET;
+        admitted = !(a.use_violate && violate) && !(a.use_meet && !ok);
+        if (admitted) flags |= STRAIT_PAIR_FEASIBLE;
       }
-      e.cmp = ent[(2 * NM + 0) * tg.TT + tid];
-      e.mem = ent[(2 * NM + 1) * tg.TT + tid];
-      e.tk = ent[(2 * NM + 2) * tg.TT + tid];
-      e.dl = ent[(2 * NM + 3) * tg.TT + tid];
-      e.ks = ent[(2 * NM + 4) * tg.TT + tid];
-      e.prio = ((const int8_t*)(stage + L.eprio))[tid];
+      const int64_t p = tile * TP + pl;
+      if (a.pair_flags) a.pair_flags[p] = flags;
+      if (a.pair_latency) __stcs(a.pair_latency + p, lat);
+      if (a.pair_intf) __stcs(a.pair_intf + p, intf);
+      s_lat[pl] = lat;
+      s_intf[pl] = intf;
+      s_adm[pl] = admitted;
     }
-    tile_compute<NM, C>(a, tg, L, CL, smem, stage, tile * tg.spb, e);  // ends with a group barrier
-    // stage `st` is fully consumed: refill it with tile k + nstages
-    if (tid == 0) {
-      const int64_t tt = tile + (int64_t)nstages * gridDim.x;
-      if (tt < ntiles) issue_tile_tma<NM, C>(a, tg, L, stage, &bars[st], tt, pol);
+
+    // ---- 3. last warp of the tile: best_for argmin per segment ----
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atomicAdd((int*)(stage + W.cnt), 1) == 7;
     }
-    if (cand_thread) {
-      unsigned char* nst = smem + ((k + 1) % nstages) * L.bytes;
-      if (tid < ncand) ((double*)(nst + L.cand))[tid] = cnext;
-      else ((int8_t*)(nst + L.cprio))[tid - ncand] = pnext;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
+      for (int q = 0; q < spb; ++q) {
+        ArgminKey key{INT_MAX, 0.0, INT_MAX, 0.0};
+        for (int gg = lane; gg < G; gg += 32) {
+          const int qp = q * G + gg;
+          if (!s_adm[qp]) continue;
+          const double lt = s_lat[qp];
+          ArgminKey en{gg, lt, INT_MAX, 0.0};
+          if (!isnan(lt)) {
+            en.best_g = gg;
+            en.best_lat = lt;
+          }
+          key = argmin_combine(key, en);
+        }
+        key = argmin_warp(key);
+        if (lane == 0) {
+          const int64_t s = tile * spb + q;
+          int bg = -1;
+          if (key.first_g != INT_MAX) bg = isnan(key.first_lat) ? key.first_g : key.best_g;
+          a.seg_gpu[s] = bg;
+          a.seg_latency[s] = bg >= 0 ? s_lat[q * G + bg] : nan;
+          a.seg_intf[s] = bg >= 0 ? s_intf[q * G + bg] : nan;
+        }
+      }
+      if (lane == 0) *(int*)(stage + W.cnt) = 0;
     }
-    group_sync(kSweepThreads);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
 }
 
@@ -550,7 +717,8 @@ static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
 // TMA eligibility: whole tiles, 16-byte aligned chunk offsets and sizes.
 static bool tma_eligible(const StraitSweepArgs& a, const TileGeom& tg) {
-  if (a.n_segments % tg.spb) return false;
+  if (a.n_segments % tg.spb || a.n_segments % 4) return false;
+  if (!aligned16(a.cand_prio)) return false;
   if (tg.TT % 16 || tg.TP % 16) return false;
   const void* ptrs[] = {a.ent_contrib, a.ent_twa, a.ent_self_cmp, a.ent_self_mem, a.ent_t_kernel,
                         a.ent_deadline_abs, a.ent_kstart, a.ent_prio, a.gpu_agg, a.gpu_lp_agg,
@@ -560,7 +728,54 @@ static bool tma_eligible(const StraitSweepArgs& a, const TileGeom& tg) {
   return true;
 }
 
-static int g_last_sweep_path = 0;  // 1 sync, 2 tma (diagnostics)
+static int g_last_sweep_path = 0;  // 1 sync, 2 bulk-copy pipeline, 3 tensor-map pipeline
+
+static PFN_cuTensorMapEncodeTiled encode_fn() {
+  static PFN_cuTensorMapEncodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled)p;
+  }
+  return fn;
+}
+
+// Rows base, base + stride, ... (nrows arrays of `n` doubles) as one 2-D tensor map with a
+// box of `box` columns x nrows rows.  Returns false if the arrays are not uniformly packed.
+static bool encode_rows(CUtensorMap* map, const double* const* rows, int nrows, int64_t n, int box) {
+  const int64_t stride = rows[1] - rows[0];
+  if (stride < n || n >= (1LL << 31)) return false;
+  for (int i = 1; i < nrows; ++i)
+    if (rows[i] - rows[i - 1] != stride) return false;
+  if (((uintptr_t)rows[0] & 15) || (stride * 8) % 16) return false;
+  PFN_cuTensorMapEncodeTiled enc = encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)nrows};
+  cuuint64_t strides[1] = {(cuuint64_t)(stride * 8)};
+  cuuint32_t boxd[2] = {(cuuint32_t)box, (cuuint32_t)nrows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)rows[0], dims, strides, boxd, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int NM>
+static bool packed_tensor_maps(const StraitSweepArgs& a, const TileGeom& tg, CUtensorMap* ent, CUtensorMap* pair) {
+  const int64_t Pn = a.n_segments * tg.G, Tn = Pn * tg.C;
+  const double* er[2 * NM + 5];
+  for (int m = 0; m < NM; ++m) er[m] = a.ent_contrib + m * Tn, er[NM + m] = a.ent_twa + m * Tn;
+  er[2 * NM] = a.ent_self_cmp, er[2 * NM + 1] = a.ent_self_mem, er[2 * NM + 2] = a.ent_t_kernel;
+  er[2 * NM + 3] = a.ent_deadline_abs, er[2 * NM + 4] = a.ent_kstart;
+  // the metric-major fields are themselves rows of stride Tn: require one uniform stride
+  const double* pr[2 * NM + 2];
+  for (int m = 0; m < NM; ++m) pr[m] = a.gpu_agg + m * Pn, pr[NM + m] = a.gpu_lp_agg + m * Pn;
+  pr[2 * NM] = a.gpu_cap_pct, pr[2 * NM + 1] = a.gpu_t_avail;
+  return encode_rows(ent, er, 2 * NM + 5, Tn, tg.TT) && encode_rows(pair, pr, 2 * NM + 2, Pn, tg.TP);
+}
 
 template <int NM, int C>
 static int launch_sweep_c(const StraitSweepArgs& a, cudaStream_t st, const StraitRefitArgs* r) {
@@ -568,27 +783,39 @@ static int launch_sweep_c(const StraitSweepArgs& a, cudaStream_t st, const Strai
   const StageLayout<NM> L(tg);
   const int with_refit = r ? 1 : 0;
   StraitRefitArgs rr = r ? *r : StraitRefitArgs{};
-  const int force = env_int("STRAIT_SWEEP_PATH", 0);  // 0 auto, 1 sync, 2 tma
+  const int force = env_int("STRAIT_SWEEP_PATH", 0);  // 0 auto, 1 sync, 3 bulk copies without tensor maps
   const bool use_tma = force == 1 ? false : tma_eligible(a, tg);
   if (use_tma) {
     int ns = env_int("STRAIT_SWEEP_STAGES", 2);
-    ns = ns < 1 ? 1 : (ns > kMaxStages ? kMaxStages : ns);
-    const CtaLayout<NM> CL(tg, L, ns);
-    const size_t smem = CL.bytes;
-    auto kern = sweep_tma_kernel<NM, C>;
+    ns = ns < 2 ? 2 : (ns > kWsMaxStages ? kWsMaxStages : ns);
+    int groups = env_int("STRAIT_SWEEP_GROUPS", 1);
+    groups = groups < 1 ? 1 : (groups > 2 ? 2 : groups);
+    const WsLayout<NM> WL(tg, ns);
+    const size_t smem = WL.bytes;
+    auto kern = sweep_ws_kernel<NM, C, 0>;
+    if constexpr (NM == 5) {  // the profiled shape: static one-segment tiles
+      if (tg.span == 256) kern = sweep_ws_kernel<NM, C, 256 / C>;
+    }
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return set_error(STRAIT_ECUDA, "strait_sweep: %zu B shared memory per CTA unavailable", smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    const int threads = 32 * (8 * groups + 2);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kSweepThreads + 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
     if (occ < 1) occ = 1;
     const int64_t ntiles = a.n_segments / tg.spb;
     int64_t grid = (int64_t)sm_count() * occ;
     const int cap = env_int("STRAIT_SWEEP_GRID", 0);
     if (cap > 0 && cap < grid) grid = cap;
     if (grid > ntiles) grid = ntiles;
-    if (with_refit && grid < 1) grid = 1;
-    kern<<<(unsigned)grid, kSweepThreads + 32, smem, st>>>(a, rr, with_refit, ns);
-    g_last_sweep_path = 2;
+    if (grid < 1) grid = 1;
+    CUtensorMap ent_map, pair_map;
+    memset(&ent_map, 0, sizeof ent_map);
+    memset(&pair_map, 0, sizeof pair_map);
+    const int use_tmap = force != 3 && packed_tensor_maps<NM>(a, tg, &ent_map, &pair_map) ? 1 : 0;
+    kern<<<(unsigned)grid, threads, smem, st>>>(a, rr, with_refit, ns, groups, env_int("STRAIT_SWEEP_DIAG", 0),
+                                                ent_map, pair_map, use_tmap);
+    g_last_sweep_path = use_tmap ? 3 : 2;
   } else {
     const CtaLayout<NM> CL(tg, L, 1);
     const size_t smem = CL.bytes;

@@ -23,6 +23,11 @@ METRIC_FIELDS = {"cand_contrib", "gpu_agg", "gpu_lp_agg", "ent_contrib", "ent_tw
 OUT_DTYPES = {"pair_flags": torch.uint8, "pair_latency": torch.float64, "pair_intf": torch.float64,
               "seg_gpu": torch.int32, "seg_latency": torch.float64, "seg_intf": torch.float64}
 INPUT_FIELDS = SWEEP_CAND_FIELDS + SWEEP_PAIR_FIELDS + SWEEP_ENT_FIELDS
+# packed device blocks (row order = the kernel's stage layout)
+ENT_BLOCK, PAIR_BLOCK = "ent", "pair"
+ENT_ROWS = ("ent_contrib", "ent_twa", "ent_self_cmp", "ent_self_mem", "ent_t_kernel", "ent_deadline_abs",
+            "ent_kstart")
+PAIR_ROWS = ("gpu_agg", "gpu_lp_agg", "gpu_cap_pct", "gpu_t_avail")
 
 
 @dataclass
@@ -47,11 +52,27 @@ class SweepSoA:
         return SweepSoA(self.n_metrics, self.n_slots, self.gpus_per_segment, self.concurrency_limit,
                         self.n_segments, self.now, arrays)
 
-    def to_device(self, pinned_stage: bool = False) -> "SweepSoA":
+    def to_device(self) -> "SweepSoA":
+        """Device copy in the PACKED layout: the triple fields are rows of one
+        [2*nm+5, T] block and the pair fields rows of one [2*nm+2, P] block, so the
+        sweep can move a tile with two 2-D TMA tensor copies."""
         out = {}
+        nm = self.n_metrics
+        for block, fields, n in ((ENT_BLOCK, ENT_ROWS, self.n_triples), (PAIR_BLOCK, PAIR_ROWS, self.n_pairs)):
+            rows = sum(nm if f in METRIC_FIELDS else 1 for f in fields)
+            buf = D.empty((rows, n))
+            r = 0
+            for f in fields:
+                k = nm if f in METRIC_FIELDS else 1
+                view = buf[r:r + k] if k > 1 or f in METRIC_FIELDS else buf[r]
+                view.copy_(torch.from_numpy(np.ascontiguousarray(self.arrays[f], dtype=np.float64))
+                           if not isinstance(self.arrays[f], torch.Tensor) else self.arrays[f])
+                out[f] = view
+                r += k
         for k in INPUT_FIELDS:
-            dt = torch.int8 if k in INT8_FIELDS else torch.float64
-            out[k] = D.dev(self.arrays[k], dt)
+            if k not in out:
+                dt = torch.int8 if k in INT8_FIELDS else torch.float64
+                out[k] = D.dev(self.arrays[k], dt)
         return self.like(out)
 
     def input_bytes(self) -> int:
@@ -126,4 +147,4 @@ def sweep(soa: SweepSoA, params, effect_cap: float = 50.0, use_violate: bool = T
 
 
 def last_sweep_path() -> str:
-    return {1: "sync", 2: "tma"}.get(D.lib().strait_last_sweep_path(), "none")
+    return {1: "sync", 2: "tma-bulk", 3: "tma-tensor"}.get(D.lib().strait_last_sweep_path(), "none")
