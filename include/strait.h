@@ -53,8 +53,15 @@ int strait_abi_version(void);
 const char *strait_last_error(void);
 /* number of device kernels this library launched since load (evidence counter) */
 int64_t strait_kernel_launches(void);
-/* which sweep kernel the last strait_sweep/strait_round used: 1 synchronous, 2 TMA pipeline */
+/* which sweep kernel the last strait_sweep/strait_round used:
+ * 1 synchronous, 2 bulk-copy pipeline, 3 tensor-map pipeline */
 int strait_last_sweep_path(void);
+
+/* HOST utility for input preparation: y[i] = exp(x[i]) with the host C
+ * library, i.e. the same libm call as Python's math.exp — used to turn the
+ * reference's normal draws into its lognormal batch noise exactly
+ * (simulation.py:309-311).  Not a device path. */
+void strait_host_exp(const double *x, double *y, int64_t n);
 
 /*
  * R1-R3: batched predict_interference (predictor.py:208-216).

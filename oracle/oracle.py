@@ -32,6 +32,10 @@ def lib():
         _lib.oracle_estimate_latency.argtypes = [vp, C.c_int32, C.c_double] + [vp] * 9 + [C.c_int64, vp, vp]
         _lib.oracle_sweep.argtypes = [C.POINTER(SweepArgs), C.c_int, C.c_int64, C.c_int64]
         _lib.oracle_refit.argtypes = [C.POINTER(RefitArgs)]
+        from paper_2604_28175_b200._replay_abi import ReplayArgs
+
+        _lib.oracle_replay.argtypes = [C.POINTER(ReplayArgs), C.c_int]
+        _lib.oracle_replay.restype = C.c_int
     return _lib
 
 
@@ -116,3 +120,23 @@ def refit(state, step, samples, *, nm, cap=50.0, lr=0.0075, beta1=0.7, beta2=0.9
     a.out_predicted, a.out_residual, a.out_flags = _p(pred), _p(res), _p(flags)
     lib().oracle_refit(C.byref(a))
     return state, int(stepa[0]), pred, res, flags
+
+
+def replay(batch, threads=1):
+    """Reference discrete-event replay (oracle/strait_replay_oracle.c) of a
+    paper_2604_28175_b200.replay.ReplayBatch on host buffers."""
+    from paper_2604_28175_b200.replay import ReplayResult
+
+    inputs = batch.host_inputs()
+    inputs["pred_state"] = inputs["pred_state"].copy()
+    inputs["pred_step"] = inputs["pred_step"].copy()
+    outputs = batch.alloc_outputs(device=False)
+
+    def ptr(a):
+        return C.addressof(a) if isinstance(a, C.Array) else a.ctypes.data
+
+    args = batch.args(inputs, outputs, ptr)
+    lib().oracle_replay(C.byref(args), int(threads))
+    outputs["pred_state"] = inputs["pred_state"]
+    outputs["pred_step"] = inputs["pred_step"]
+    return ReplayResult(batch, outputs)

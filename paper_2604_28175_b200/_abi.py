@@ -148,6 +148,8 @@ def _declare(lib):
     lib.strait_refit.argtypes = [C.POINTER(RefitArgs), _vp]
     lib.strait_round.restype = C.c_int
     lib.strait_round.argtypes = [C.POINTER(SweepArgs), C.POINTER(RefitArgs), _vp]
+    lib.strait_host_exp.restype = None
+    lib.strait_host_exp.argtypes = [_vp, _vp, C.c_int64]
     if hasattr(lib, "strait_replay"):
         from ._replay_abi import declare_replay
 
@@ -178,6 +180,20 @@ def check(status: int) -> None:
     if status == STRAIT_OK:
         return
     msg = lib().strait_last_error().decode(errors="replace")
+    if status == STRAIT_EINVAL:
+        raise ValueError(msg)
+    if status == STRAIT_ERUNTIME:
+        raise RuntimeError(msg)
+    if status == STRAIT_EORDER:
+        raise SimulationOrderError(msg)
+    raise StraitCudaError(msg)
+
+
+def check_code(status: int, context: str = "") -> None:
+    """Raise the reference's exception for a per-replay/per-item status code."""
+    if status == STRAIT_OK:
+        return
+    msg = f"{context}: status {status}"
     if status == STRAIT_EINVAL:
         raise ValueError(msg)
     if status == STRAIT_ERUNTIME:

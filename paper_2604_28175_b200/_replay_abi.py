@@ -1,0 +1,51 @@
+"""ctypes mirror of include/strait_replay.h."""
+from __future__ import annotations
+
+import ctypes as C
+
+from ._abi import MAX_METRICS
+
+_vp = C.c_void_p
+
+RC = dict(ERROR=0, BATCHES=1, COMPLETED=2, PASSES=3, CAP_ROWS=4, EVENTS=5, HP_ARR=6, LP_ARR=7, HP_VIOL=8,
+          LP_VIOL=9, HP_DROP=10, LP_DROP=11, RESOLVED=12)
+RC_N = 16
+
+
+class ReplayModels(C.Structure):
+    _fields_ = [("n_models", C.c_int32), ("n_metrics", C.c_int32), ("stride", C.c_int32), ("pad", C.c_int32),
+                ("max_batch", _vp), ("prio", _vp), ("deadline", _vp), ("timeout", _vp), ("total", _vp),
+                ("transfer", _vp), ("kernel", _vp), ("self_cmp", _vp), ("self_mem", _vp), ("throughput", _vp)]
+
+
+class ReplayConfig(C.Structure):
+    _fields_ = [("n_gpus", C.c_int32), ("concurrency_limit", C.c_int32), ("use_priority_order", C.c_int32),
+                ("use_meet", C.c_int32), ("use_violate", C.c_int32), ("gt_family", C.c_int32),
+                ("has_noise", C.c_int32), ("pad", C.c_int32),
+                ("effect_cap", C.c_double), ("learning_rate", C.c_double), ("beta1", C.c_double),
+                ("beta2", C.c_double), ("eps", C.c_double), ("huber_delta", C.c_double),
+                ("gt_scale", C.c_double), ("gt_base", C.c_double), ("gt_offset", C.c_double),
+                ("gt_w_cmp", C.c_double), ("gt_w_mem", C.c_double), ("gt_pf_high", C.c_double),
+                ("gt_pf_low", C.c_double), ("gt_w", C.c_double * MAX_METRICS),
+                ("aimd_floor", C.c_double), ("aimd_ceiling", C.c_double), ("aimd_increase", C.c_double),
+                ("aimd_interval", C.c_double)]
+
+
+ARG_ARRAYS = ["cfg", "req_off", "arr_time", "arr_model", "model_req", "mr_off", "noise", "bc1", "bc2",
+              "pred_state", "pred_step", "req_status", "req_violated", "req_completion", "req_batch",
+              "dec_time", "dec_pass", "dec_model", "dec_size", "dec_gpu", "dec_est_latency", "dec_intf",
+              "b_front", "b_transfer_start", "b_transfer_end", "b_kernel_start", "b_kernel_end", "b_completion",
+              "b_work", "b_done_order", "fb_predicted", "fb_actual", "fb_residual", "fb_flags",
+              "cap_time", "cap_gpu", "cap_pct", "counters"]
+
+
+class ReplayArgs(C.Structure):
+    _fields_ = [("n_replays", C.c_int32), ("cap_rows_max", C.c_int32), ("n_bc", C.c_int32), ("pad", C.c_int32),
+                ("models", ReplayModels)] + [(k, _vp) for k in ARG_ARRAYS]
+
+
+def declare_replay(lib):
+    lib.strait_replay.restype = C.c_int
+    lib.strait_replay.argtypes = [C.POINTER(ReplayArgs), _vp]
+    lib.strait_replay_smem_bytes.restype = C.c_int64
+    lib.strait_replay_smem_bytes.argtypes = [C.c_int32] * 4

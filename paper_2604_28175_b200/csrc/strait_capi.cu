@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 
@@ -35,3 +36,7 @@ int check_launch(const char* what) {
 extern "C" int strait_abi_version(void) { return STRAIT_ABI_VERSION; }
 extern "C" const char* strait_last_error(void) { return g_err; }
 extern "C" int64_t strait_kernel_launches(void) { return g_launches.load(); }
+
+extern "C" void strait_host_exp(const double* x, double* y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = ::exp(x[i]);
+}

@@ -1,0 +1,266 @@
+"""Batched trace replays on the device (reference: infersim/simulation.py).
+
+``ReplayBatch`` turns (ExperimentConfig, seed[, predictor]) replays into the
+flat host arrays of include/strait_replay.h — arrival streams and batch noise
+drawn exactly as the reference draws them — and ``ReplayBatch.run()``
+executes every replay to completion in ONE launch of the CUDA engine
+(strait_replay, one warp per replay).  Results come back as numpy arrays;
+``ReplayResult.sim_result(r)`` rebuilds the reference's row schemas.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _device as D
+from ._replay_abi import ARG_ARRAYS, RC, RC_N, ReplayArgs, ReplayConfig, ReplayModels
+from .config import ExperimentConfig
+from .domain import PriorityLevel
+from .predictor import InterferencePredictor, PredictorParams, bias_correction_tables
+
+NOISE_STREAM = 1_000_003  # simulation.py:163
+
+# output arrays: name -> (dtype, per) with per in {"req", "batch", "cap", "replay"}
+OUTPUTS = {
+    "req_status": (np.int8, "req"), "req_violated": (np.uint8, "req"), "req_completion": (np.float64, "req"),
+    "req_batch": (np.int32, "req"),
+    "dec_time": (np.float64, "req"), "dec_pass": (np.int32, "req"), "dec_model": (np.int16, "req"),
+    "dec_size": (np.int8, "req"), "dec_gpu": (np.int16, "req"), "dec_est_latency": (np.float64, "req"),
+    "dec_intf": (np.float64, "req"), "b_front": (np.float64, "req"), "b_transfer_start": (np.float64, "req"),
+    "b_transfer_end": (np.float64, "req"), "b_kernel_start": (np.float64, "req"),
+    "b_kernel_end": (np.float64, "req"), "b_completion": (np.float64, "req"), "b_work": (np.float64, "req"),
+    "b_done_order": (np.int32, "req"), "fb_predicted": (np.float64, "req"), "fb_actual": (np.float64, "req"),
+    "fb_residual": (np.float64, "req"), "fb_flags": (np.uint8, "req"),
+    "cap_time": (np.float64, "cap"), "cap_gpu": (np.int16, "cap"), "cap_pct": (np.float64, "cap"),
+    "counters": (np.int64, "replay"),
+}
+
+
+@dataclass
+class ReplaySpec:
+    config: ExperimentConfig
+    seed: Optional[int] = None
+    predictor: Optional[InterferencePredictor] = None
+
+
+def host_exp(x: np.ndarray) -> np.ndarray:
+    """exp with the host libm (same call as Python's math.exp)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    D.lib().strait_host_exp(x.ctypes.data, y.ctypes.data, x.size)
+    return y
+
+
+def model_tables(profiles: dict) -> dict:
+    ids = sorted(profiles)
+    M = len(ids)
+    nm = len(profiles[ids[0]].metrics)
+    B = max(p.max_batch_size for p in profiles.values())
+    t = {k: np.zeros(M * B) for k in ("total", "transfer", "kernel", "self_cmp", "self_mem")}
+    thr = np.zeros((nm, M * B))
+    for m, mid in enumerate(ids):
+        p = profiles[mid]
+        n = p.max_batch_size
+        t["total"][m * B:m * B + n] = p.total_latency
+        t["transfer"][m * B:m * B + n] = p.transfer_latency
+        t["kernel"][m * B:m * B + n] = p.kernel_latency
+        t["self_cmp"][m * B:m * B + n] = p.self_compute
+        t["self_mem"][m * B:m * B + n] = p.self_memory
+        thr[:, m * B:m * B + n] = np.asarray(p.throughput, dtype=np.float64).T
+    t["throughput"] = thr
+    t["max_batch"] = np.array([profiles[i].max_batch_size for i in ids], dtype=np.int32)
+    t["prio"] = np.array([int(profiles[i].priority) for i in ids], dtype=np.int8)
+    t["deadline"] = np.array([profiles[i].deadline_ms for i in ids], dtype=np.float64)
+    t["timeout"] = np.array([profiles[i].batch_timeout_ms for i in ids], dtype=np.float64)
+    return dict(ids=ids, M=M, nm=nm, B=B, **t)
+
+
+def replay_config(cfg: ExperimentConfig, pred: InterferencePredictor) -> ReplayConfig:
+    if cfg.policy != "predictive":
+        raise NotImplementedError(f"device replay implements the predictive policy, got {cfg.policy!r}")
+    variant = cfg.policy_variant
+    gt = cfg.ground_truth.without_priority_advantage() if variant == "no_gamma_advantage" else cfg.ground_truth
+    c = ReplayConfig()
+    c.n_gpus, c.concurrency_limit = cfg.n_gpus, cfg.concurrency_limit
+    c.use_priority_order = int(variant != "no_priority_scan")
+    c.use_meet = int(variant != "no_meet")
+    c.use_violate = int(variant != "no_violate_aimd")
+    c.gt_family = 0 if gt.family == "exponential" else 1
+    c.has_noise = int(gt.noise_sigma > 0)
+    c.effect_cap = pred.params.effect_cap
+    o = pred.opt
+    c.learning_rate, c.beta1, c.beta2, c.eps, c.huber_delta = o.learning_rate, o.beta1, o.beta2, o.eps, o.huber_delta
+    c.gt_scale, c.gt_base, c.gt_offset = gt.scale, gt.base, gt.offset
+    c.gt_w_cmp, c.gt_w_mem = gt.self_compute_weight, gt.self_memory_weight
+    c.gt_pf_high, c.gt_pf_low = gt.priority_factor[PriorityLevel.HIGH], gt.priority_factor[PriorityLevel.LOW]
+    for i, w in enumerate(gt.weights):
+        c.gt_w[i] = w
+    a = cfg.aimd
+    c.aimd_floor, c.aimd_ceiling, c.aimd_increase, c.aimd_interval = a.floor, a.ceiling, a.increase_pct, a.interval_ms
+    return c
+
+
+class ReplayBatch:
+    """Host inputs of a batch of replays sharing one profile set."""
+
+    def __init__(self, specs: Sequence[ReplaySpec], cap_rows_max: Optional[int] = None):
+        if not specs:
+            raise ValueError("empty replay batch")
+        self.specs = list(specs)
+        prof = self.specs[0].config.profiles
+        for s in self.specs:
+            s.config.validate()
+            if sorted(s.config.profiles) != sorted(prof):
+                raise ValueError("all replays of a batch must share one profile set")
+        self.tab = model_tables(prof)
+        M, nm = self.tab["M"], self.tab["nm"]
+        self.preds = []
+        arr_t, arr_m, model_req, mr_off, noise, req_off, cfgs, states, steps = [], [], [], [0], [], [0], [], [], []
+        for s in self.specs:
+            cfg = s.config
+            seed = cfg.seed if s.seed is None else s.seed
+            pred = s.predictor or InterferencePredictor(PredictorParams(weights=(0.1,) * nm))
+            self.preds.append(pred)
+            streams = cfg.workload.generate_arrays(seed)
+            per = [np.asarray(streams.get(mid, np.empty(0)), dtype=np.float64) for mid in self.tab["ids"]]
+            counts = np.array([len(x) for x in per], dtype=np.int64)
+            times = np.concatenate(per) if len(per) else np.empty(0)
+            models = np.repeat(np.arange(M, dtype=np.int16), counts)
+            order = np.argsort(times, kind="stable")  # heap order: (time, model-sorted k seq)
+            pos = np.empty(len(times), dtype=np.int64)
+            pos[order] = np.arange(len(times))
+            base = req_off[-1]
+            arr_t.append(times[order])
+            arr_m.append(models[order])
+            model_req.append((pos + base).astype(np.int32))
+            starts = np.concatenate([[0], np.cumsum(counts)])
+            mr_off.extend((base + starts[1:]).tolist())
+            n = len(times)
+            if cfg.ground_truth.noise_sigma > 0 and n:
+                rng = np.random.default_rng(np.random.SeedSequence([seed, NOISE_STREAM]))
+                noise.append(host_exp(rng.normal(0.0, cfg.ground_truth.noise_sigma, n)))
+            else:
+                noise.append(np.ones(n))
+            req_off.append(base + n)
+            cfgs.append(replay_config(cfg, pred))
+            states.append(pred.params.to_vector() + list(pred.opt.m) + list(pred.opt.v))
+            steps.append(pred.opt.step)
+        betas = {(p.opt.beta1, p.opt.beta2) for p in self.preds}
+        if len(betas) != 1:
+            raise ValueError("all replays of a batch must share the Adam betas")
+        b1, b2 = betas.pop()
+        N = req_off[-1]
+        bc1, bc2 = bias_correction_tables(b1, b2, max(steps) + N + 1)
+        self.N = int(N)
+        self.R = len(self.specs)
+        if cap_rows_max is None:
+            cap_rows_max = max(
+                s.config.n_gpus * (2 * (int(s.config.workload.duration_ms / s.config.aimd.interval_ms) + 400) + 3)
+                for s in self.specs)
+        self.cap_rows_max = int(cap_rows_max)
+        self.inputs = {
+            "req_off": np.asarray(req_off, dtype=np.int64),
+            "arr_time": np.concatenate(arr_t), "arr_model": np.concatenate(arr_m),
+            "model_req": np.concatenate(model_req), "mr_off": np.asarray(mr_off, dtype=np.int64),
+            "noise": np.concatenate(noise), "bc1": bc1, "bc2": bc2,
+            "pred_state": np.asarray(states, dtype=np.float64).ravel(),
+            "pred_step": np.asarray(steps, dtype=np.int64),
+            "cfg": (ReplayConfig * self.R)(*cfgs),
+        }
+
+    # ------------------------------------------------------------------ buffers
+    def alloc_outputs(self, device: bool):
+        sizes = {"req": max(self.N, 1), "cap": self.R * self.cap_rows_max, "replay": self.R * RC_N}
+        out = {}
+        for k, (dt, per) in OUTPUTS.items():
+            if device:
+                out[k] = D.empty(sizes[per], getattr(torch, np.dtype(dt).name))
+            else:
+                out[k] = np.zeros(sizes[per], dtype=dt)
+        return out
+
+    def args(self, inputs: dict, outputs: dict, ptr) -> ReplayArgs:
+        a = ReplayArgs()
+        a.n_replays, a.cap_rows_max, a.n_bc = self.R, self.cap_rows_max, len(self.inputs["bc1"])
+        t = self.tab
+        md = a.models
+        md.n_models, md.n_metrics, md.stride = t["M"], t["nm"], t["B"]
+        for k in ("max_batch", "prio", "deadline", "timeout", "total", "transfer", "kernel", "self_cmp",
+                  "self_mem", "throughput"):
+            setattr(md, k, ptr(inputs["tab_" + k]))
+        for k in ARG_ARRAYS:
+            src = outputs if k in outputs else inputs
+            setattr(a, k, ptr(src[k]))
+        return a
+
+    def host_inputs(self) -> dict:
+        d = dict(self.inputs)
+        for k in ("max_batch", "prio", "deadline", "timeout", "total", "transfer", "kernel", "self_cmp",
+                  "self_mem", "throughput"):
+            d["tab_" + k] = np.ascontiguousarray(self.tab[k])
+        return d
+
+    def device_inputs(self) -> dict:
+        out = {}
+        for k, v in self.host_inputs().items():
+            if k == "cfg":
+                buf = np.frombuffer(bytes(v), dtype=np.uint8)
+                out[k] = D.dev(buf, torch.uint8)
+            else:
+                out[k] = D.dev(v, getattr(torch, np.asarray(v).dtype.name))
+        return out
+
+    def run(self, stream=None) -> "ReplayResult":
+        """Host in, one device launch, host out."""
+        din = self.device_inputs()
+        dout = self.alloc_outputs(device=True)
+        args = self.args(din, dout, D.ptr)
+        D.check(D.lib().strait_replay(C.byref(args), D.stream_handle(stream)))
+        res = {k: D.host(v) for k, v in dout.items()}
+        res["pred_state"] = D.host(din["pred_state"])
+        res["pred_step"] = D.host(din["pred_step"])
+        return ReplayResult(self, res)
+
+
+class ReplayResult:
+    """Outputs of a replay batch (numpy), with reference-shaped views."""
+
+    def __init__(self, batch: ReplayBatch, arrays: dict):
+        self.batch = batch
+        self.a = arrays
+        self.counters = arrays["counters"].reshape(batch.R, RC_N)
+
+    def check(self):
+        from ._abi import check_code
+
+        for r in range(self.batch.R):
+            check_code(int(self.counters[r, RC["ERROR"]]), f"replay {r}")
+
+    def violation_rates(self, r: int) -> tuple[float, float]:
+        c = self.counters[r]
+        hp = 100.0 * c[RC["HP_VIOL"]] / c[RC["HP_ARR"]] if c[RC["HP_ARR"]] else 0.0
+        lp = 100.0 * c[RC["LP_VIOL"]] / c[RC["LP_ARR"]] if c[RC["LP_ARR"]] else 0.0
+        return hp, lp
+
+    def replay_slice(self, r: int) -> dict:
+        """Per-replay views: request arrays (global order) and batch arrays (submission order)."""
+        b = self.batch
+        lo, hi = int(b.inputs["req_off"][r]), int(b.inputs["req_off"][r + 1])
+        nb = int(self.counters[r, RC["BATCHES"]])
+        out = {}
+        for k, (_, per) in OUTPUTS.items():
+            if per == "req":
+                out[k] = self.a[k][lo:hi] if k.startswith("req") else self.a[k][lo:lo + nb]
+            elif per == "cap":
+                n = min(int(self.counters[r, RC["CAP_ROWS"]]), b.cap_rows_max)
+                out[k] = self.a[k][r * b.cap_rows_max:r * b.cap_rows_max + n]
+        np_ = b.tab["nm"] + 7
+        out["pred_state"] = self.a["pred_state"][r * 3 * np_:(r + 1) * 3 * np_]
+        out["pred_step"] = int(self.a["pred_step"][r])
+        out["counters"] = self.counters[r]
+        return out

@@ -271,8 +271,167 @@ def gen_twa():
                            for k, v in rows.items()})
 
 
+# ----------------------------------------------------------------------------- replays
+C1_DOC = {"profiles": "default6", "duration_ms": 26316, "seed": 1, "n_gpus": 1, "policy": "predictive",
+          "ground_truth": {"noise_sigma": 0.05},
+          "workload": {"resnet50": {"mode": "poisson", "rate": 300}, "roberta_b": {"mode": "poisson", "rate": 80}}}
+OVERLOAD_GT = {"family": "exponential", "scale": 0.5, "base": 2.718281828459045, "offset": -0.7686,
+               "weights": [0.3] * 5, "self_compute_weight": 0.25, "self_memory_weight": 0.2,
+               "priority_factor": {"high": 0.6, "low": 1.0}, "noise_sigma": 0.05}
+OVERLOAD_WL = {"resnet50": {"mode": "poisson", "rate": 2200}, "vit_b16": {"mode": "poisson", "rate": 800},
+               "yolo_v8n": {"mode": "poisson", "rate": 1300}, "convnext_b": {"mode": "poisson", "rate": 650},
+               "vgg19": {"mode": "poisson", "rate": 650}, "roberta_b": {"mode": "poisson", "rate": 400}}
+
+
+def overload_doc(duration, **kw):
+    d = {"profiles": "default6", "duration_ms": duration, "seed": 0, "n_gpus": 4, "concurrency_limit": 4,
+         "policy": "predictive", "goodput_window_ms": 1000, "ground_truth": dict(OVERLOAD_GT),
+         "workload": dict(OVERLOAD_WL)}
+    d.update(kw)
+    return d
+
+
+def c5_slice_doc(tmpdir, duration=150):
+    """C5 shape: 64 GPUs, 20 random profiles, bursty HP trace + LP Poisson."""
+    import infersim.profiles as RP
+    rng = np.random.default_rng(2604)
+    profs = {f"m{i:02d}": RP.random_profile(rng, f"m{i:02d}", PriorityLevel.HIGH if i < 6 else PriorityLevel.LOW)
+             for i in range(20)}
+    pdir = os.path.join(tmpdir, "c5_profiles")
+    RP.save_profiles_dir(profs, pdir)
+    trace = os.path.join(tmpdir, "c5_trace.csv")
+    with open(trace, "w") as f:
+        f.write("function_id,minute_index,count\n")
+        for i in range(6):
+            for m in range(2):
+                f.write(f"hp{i},{m},{int(rng.lognormal(math.log(150000), 0.6))}\n")
+    wl = {f"m{i:02d}": ({"mode": "trace", "trace_file": trace, "function_id": f"hp{i}", "scale": 1.0} if i < 6
+                        else {"mode": "poisson", "rate": 2600}) for i in range(20)}
+    return {"profiles": pdir, "duration_ms": duration, "seed": 0, "n_gpus": 64, "concurrency_limit": 4,
+            "policy": "predictive", "ground_truth": {"noise_sigma": 0.05}, "workload": wl}
+
+
+REPLAY_CASES = {
+    "demo": ("yaml", "/root/reference/pkg/configs/demo.yaml", None),
+    "c1": ("doc", C1_DOC, None),
+    "overload": ("yaml", "/root/reference/pkg/configs/overload.yaml", None),
+    "trace": ("doc", None, "trace"),
+    "ov_no_meet": ("doc", overload_doc(500, policy_variant="no_meet"), None),
+    "ov_no_violate": ("doc", overload_doc(500, policy_variant="no_violate_aimd"), None),
+    "ov_no_prio": ("doc", overload_doc(500, policy_variant="no_priority_scan"), None),
+    "ov_no_gamma": ("doc", overload_doc(500, policy_variant="no_gamma_advantage"), None),
+    "ov_quadratic": ("doc", overload_doc(500, ground_truth=dict(OVERLOAD_GT, family="quadratic", scale=0.3,
+                                                                 offset=-0.4)), None),
+    "ov_nonoise_2gpu": ("doc", overload_doc(400, n_gpus=2, ground_truth=dict(OVERLOAD_GT, noise_sigma=0.0)), None),
+    "c5_slice": ("doc", None, "c5"),
+}
+
+
+def replay_case_docs(name, tmpdir):
+    kind, src, special = REPLAY_CASES[name]
+    if special == "trace":
+        import yaml
+        doc = yaml.safe_load(open("/root/reference/pkg/configs/trace_replay.yaml"))
+        doc["duration_ms"] = 30000
+        return doc, "/root/reference/pkg/configs"
+    if special == "c5":
+        return c5_slice_doc(tmpdir), tmpdir
+    if kind == "yaml":
+        import yaml
+        return yaml.safe_load(open(src)), os.path.dirname(src)
+    return src, "."
+
+
+def reference_replay_arrays(name, tmpdir):
+    import infersim.config as RC
+    from infersim.simulation import Simulation, parse_segments
+    from paper_2604_28175_b200 import config as MC
+    from paper_2604_28175_b200.replay import ReplayBatch, ReplaySpec
+
+    doc, base = replay_case_docs(name, tmpdir)
+    rcfg = RC.config_from_dict(doc, base_dir=base)
+    mcfg = MC.config_from_dict(doc, base_dir=base)
+    sim = Simulation(rcfg)
+    res = sim.run()
+    batch = ReplayBatch([ReplaySpec(mcfg)])
+    ids = batch.tab["ids"]
+    mr = batch.inputs["model_req"]
+    mr_off = batch.inputs["mr_off"]
+    out = {}
+    # pin the workload generator: the reference's streams, model-major
+    streams = rcfg.workload.generate(rcfg.seed)
+    ref_times = np.concatenate([np.asarray(streams.get(m, []), dtype=np.float64) for m in ids])
+    my_times = batch.inputs["arr_time"][np.argsort(mr, kind="stable")] if len(mr) else np.empty(0)
+    my_model_major = batch.inputs["arr_time"][mr]
+    assert np.array_equal(ref_times, my_model_major), f"{name}: workload streams differ"
+    del my_times
+    N = batch.N
+    st = np.zeros(N, np.int8); vi = np.zeros(N, np.uint8); comp = np.full(N, np.nan); rb = np.full(N, -1, np.int32)
+    for row in res.request_rows:
+        mid, k = row["request"].rsplit("-", 1)
+        g = mr[mr_off[ids.index(mid)] + int(k)]
+        st[g] = 2 if row["dropped"] else 1
+        vi[g] = row["violated"]
+        if not row["dropped"]:
+            comp[g] = row["completion"]
+            rb[g] = int(row["batch"][1:])
+    out.update(req_status=st, req_violated=vi, req_completion=comp, req_batch=rb)
+    D = res.decision_rows
+    out.update(dec_time=np.array([d["time"] for d in D]), dec_pass=np.array([d["pass_id"] for d in D], np.int32),
+               dec_model=np.array([ids.index(d["model"]) for d in D], np.int16),
+               dec_size=np.array([d["size"] for d in D], np.int8), dec_gpu=np.array([d["gpu"] for d in D], np.int16),
+               dec_est_latency=np.array([d["est_latency"] for d in D]),
+               dec_intf=np.array([d["intf_pred"] for d in D]))
+    nb = len(D)
+    cols = {k: np.full(nb, np.nan) for k in ("b_front", "b_transfer_start", "b_kernel_start", "b_kernel_end",
+                                              "b_completion", "b_work", "fb_predicted", "fb_actual",
+                                              "fb_residual")}
+    done = np.full(nb, -1, np.int32)
+    flags = np.zeros(nb, np.uint8)
+    for j, row in enumerate(res.batch_rows):
+        b = int(row["batch"][1:])
+        cols["b_front"][b] = row["front_enqueue"]
+        cols["b_transfer_start"][b] = row["transfer_start"]
+        cols["b_kernel_start"][b] = row["kernel_start"]
+        cols["b_kernel_end"][b] = row["kernel_end"]
+        cols["b_completion"][b] = row["completion"]
+        cols["b_work"][b] = sum(d / s for d, s in parse_segments(row["segments"]))
+        done[b] = j
+    for row in res.feedback_rows:
+        b = int(row["batch"][1:])
+        cols["fb_predicted"][b] = row["predicted"]
+        cols["fb_actual"][b] = row["actual"]
+        cols["fb_residual"][b] = row["residual"]
+        flags[b] = (1 if row["skipped"] else 0) | (2 if row["saturated"] else 0)
+    out.update(cols)
+    out.update(b_done_order=done, fb_flags=flags)
+    out.update(cap_time=np.array([c["time"] for c in res.cap_rows]),
+               cap_gpu=np.array([c["gpu"] for c in res.cap_rows], np.int16),
+               cap_pct=np.array([c["cap_pct"] for c in res.cap_rows]))
+    p = sim.predictor
+    out["pred_state"] = np.array(p.params.to_vector() + p.opt.m + p.opt.v)
+    out["pred_step"] = np.array(p.opt.step)
+    m = res.metrics.per_class
+    out["class_counts"] = np.array([[m[c].arrivals, m[c].dropped, m[c].violations] for c in PriorityLevel])
+    out["trace_hash"] = np.array(res.trace_hash())
+    return out
+
+
+def gen_replay():
+    import tempfile
+    import yaml
+    os.makedirs(os.path.join(HERE, "replay"), exist_ok=True)
+    with tempfile.TemporaryDirectory() as tmp:
+        for name in REPLAY_CASES:
+            arrays = reference_replay_arrays(name, tmp)
+            doc, _ = replay_case_docs(name, tmp)
+            np.savez_compressed(os.path.join(HERE, "replay", f"{name}.npz"), **arrays)
+            print(f"  {name}: {len(arrays['req_status'])} requests, {len(arrays['dec_time'])} batches, "
+                  f"classes {arrays['class_counts'].tolist()}", flush=True)
+
+
 if __name__ == "__main__":
-    what = sys.argv[1:] or ["predict", "latency", "refit", "sweep", "twa"]
+    what = sys.argv[1:] or ["predict", "latency", "refit", "sweep", "twa", "replay"]
     for w in what:
         print("generating", w, flush=True)
         globals()[f"gen_{w}"]()
