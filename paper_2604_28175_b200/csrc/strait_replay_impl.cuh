@@ -1,0 +1,1040 @@
+// strait_replay_impl.cuh — the device trace-replay engine (R5-R21): whole
+// discrete-event replays of the Strait scheduler, ONE WARP PER REPLAY, the
+// replay's entire mutable state resident in that warp's slice of shared
+// memory.  Instantiated once per metric count in strait_replay_nm*.cu.
+//
+// Restates /root/reference/pkg/src/infersim/simulation.py:122-513 driving
+// PredictivePolicy (scheduler.py:229-378), InterferencePredictor
+// (predictor.py:161-363), PcieLinkState (pcie.py:13-53), GpuRuntimeState +
+// AimdState (runtime.py:13-141), ThroughputTimeline (domain.py:217-264) and
+// the hidden ground truth (oracle.py:55-77).
+//
+// B200 design (not the reference's structure):
+//  * No event heap.  Every live event of a replay has a fixed home: each
+//    running-batch slot holds at most ONE pending event (its transfer-complete
+//    or its latest kernel-complete; older kernel-completes are exactly the
+//    reference's stale, version-superseded events), each model queue holds its
+//    latest batch timeout, plus one AIMD tick and the head of the pre-sorted
+//    arrival stream.  The next event is a warp-wide lexicographic argmin over
+//    these <= G*C + M + 2 candidates on the reference's (time, kind, seq) key,
+//    with seq assigned in the reference's push order, so pops happen in the
+//    reference's order and stale events never exist.
+//  * Timelines are kept in running-integral form (t0, t_last, v_last, acc):
+//    the same additions in the same order as the reference loop
+//    (domain.py:249-264), O(1) memory per running batch.
+//  * Lane-parallel: the pass's queue ordering (rank sort), early drop
+//    (ballot over the queue prefix), best_for (lane per GPU), recompute and
+//    timeline stamping (lane per running entry), the aggregate (lane per
+//    metric), the refit (lane per parameter, predictor.py:345-363), cap rows
+//    (ballot-ordered).  Everything else is uniform scalar code executed by all
+//    lanes; shared-memory scalars are written by lane 0 followed by __syncwarp.
+//  * Binary64 throughout, --fmad=false, left-to-right evaluation as the
+//    reference; the only deviation is libdevice exp/log/pow vs glibc.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/strait_replay.h"
+#include "strait_capi.cuh"
+#include "strait_device.cuh"
+
+namespace strait {
+namespace rp {
+
+constexpr int kKC = 0, kTC = 1, kARR = 2, kTO = 3, kTICK = 4;  // simulation.py:28-33 tie ranks
+constexpr double kWorkEps = 1e-9;                               // simulation.py:35
+constexpr unsigned long long kNoKey = ~0ULL;
+constexpr int kMaxConc = 8;
+constexpr int kMaxModels = 64;
+constexpr int kMaxBatch = 64;
+constexpr unsigned kFull = 0xffffffffu;
+
+__host__ __device__ __forceinline__ size_t al(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// Shared-memory layout of one replay (one warp), grouped field arrays so the
+// engine needs only a handful of base pointers.  Slot s = j * G + g is
+// running-batch slot j of GPU g (G, C = the launch's maximum geometry);
+// per-GPU fields are [field][G] so lanes over GPUs touch consecutive words.
+// Slot double fields (SD_*), then NM timeline values and NM integrals:
+enum { SD_DL, SD_KS, SD_T0, SD_TL, SD_REM, SD_SLOW, SD_NOISE, SD_LAST, SD_WORK, SD_ICUR, SD_VL };
+enum { SI_BID, SI_REQ0, SI_ICP, SI_N };
+enum { SB_MODEL, SB_SIZE, SB_PRIO, SB_STARTED, SB_LIVE, SB_TLEN, SB_N };
+enum { GD_TAV, GD_CAP, GD_TICK, GD_AGG };  // then NM aggregates, then C pending reservations
+enum { GI_NRUN, GI_PHEAD, GI_PN, GI_N };
+enum { QI_HEAD, QI_TAIL, QI_FGEN, QI_TGEN, QI_EGEN, QI_ORD, QI_N };
+
+struct Layout {
+  int G, C, M, NM, S, NE;
+  size_t P, sd, gd, ed, ek, qd, si, gi, qi, sb, go, qb, bytes;
+  __host__ __device__ static int sd_fields(int nm) { return SD_VL + 2 * nm; }
+  __host__ __device__ static int gd_fields(int nm, int c) { return GD_AGG + nm + c; }
+  __host__ __device__ Layout(int g, int c, int m, int nm) : G(g), C(c), M(m), NM(nm) {
+    S = G * C;
+    NE = S + M + 2;
+    size_t o = 0;
+    auto take = [&](size_t n) {
+      size_t r = o;
+      o = al(o + n);
+      return r;
+    };
+    P = take(8 * (NM + 7));
+    sd = take(8 * (size_t)sd_fields(NM) * S);
+    gd = take(8 * (size_t)gd_fields(NM, C) * G);
+    ed = take(8 * (size_t)NE);
+    ek = take(8 * (size_t)NE);
+    qd = take(8 * (size_t)M);
+    si = take(4 * (size_t)SI_N * S);
+    gi = take(4 * (size_t)GI_N * G);
+    qi = take(4 * (size_t)QI_N * M);
+    sb = take((size_t)SB_N * S);
+    go = take((size_t)C * G);
+    qb = take((size_t)M);
+    bytes = o;
+  }
+};
+
+template <int NM>
+struct Sim {
+  static constexpr int NP = NM + 7;
+  static constexpr int SD_ACC = SD_VL + NM;
+  static constexpr int GD_PEND = GD_AGG + NM;
+  // ---- launch-wide inputs
+  const StraitReplayArgs* A;
+  const StraitReplayConfig* cf;
+  int lane;
+  int G, C, M, B, S, NE;  // layout strides (launch maxima), models, table stride
+  int NG, CONC;           // this replay's n_gpus and concurrency_limit
+  int64_t r, base, N;     // request range [base, base + N)
+  // ---- shared-memory state: grouped field arrays of this warp's slice
+  double *P, *sd, *gd, *ed, *qd;
+  unsigned long long* ek;
+  int *si, *gi, *qi;
+  int8_t *sb, *go, *qb;
+  // ---- uniform scalar state (identical in every lane)
+  Pred<NM> pr;
+  double adam_m, adam_v;  // lane-owned Adam moments (lane k owns parameter k)
+  int64_t step;
+  unsigned long long seq;
+  int batch_seq, pass_seq, done_order, err;
+  int64_t next_arr, resolved;
+  int64_t c_batches, c_completed, c_passes, c_cap_rows, c_events, c_hp_viol, c_lp_viol, c_hp_drop, c_lp_drop;
+
+  // ------------------------------------------------------------ accessors
+  __device__ __forceinline__ double& SD(int f, int s) const { return sd[f * S + s]; }
+  __device__ __forceinline__ int& SI(int f, int s) const { return si[f * S + s]; }
+  __device__ __forceinline__ int8_t& SB(int f, int s) const { return sb[f * S + s]; }
+  __device__ __forceinline__ double& GD(int f, int g) const { return gd[f * G + g]; }
+  __device__ __forceinline__ int& GI(int f, int g) const { return gi[f * G + g]; }
+  __device__ __forceinline__ int& QI(int f, int m) const { return qi[f * M + m]; }
+  __device__ __forceinline__ int8_t& ORD(int p, int g) const { return go[p * G + g]; }
+  __device__ __forceinline__ int slot(int g, int j) const { return j * G + g; }
+  __device__ __forceinline__ int slot_at(int g, int p) const { return slot(g, ORD(p, g)); }
+
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+  template <typename T>
+  __device__ __forceinline__ void put(T& ref, T v) const {  // uniform scalar store
+    if (lane == 0) ref = v;
+  }
+  __device__ __forceinline__ void fail(int code) {
+    if (!err) err = code;
+  }
+  __device__ __forceinline__ void fail_any(bool bad, int code) {
+    if (__any_sync(kFull, bad)) fail(code);
+  }
+  // profile tables (domain.py:52-105), size k in 1..max_batch
+  __device__ __forceinline__ int64_t ti(int m, int k) const { return (int64_t)m * B + k - 1; }
+  __device__ __forceinline__ double thr(int m, int k, int i) const {
+    return __ldg(&A->models.throughput[(int64_t)i * M * B + ti(m, k)]);
+  }
+  __device__ __forceinline__ double tab_total(int m, int k) const { return __ldg(&A->models.total[ti(m, k)]); }
+  __device__ __forceinline__ double tab_transfer(int m, int k) const { return __ldg(&A->models.transfer[ti(m, k)]); }
+  __device__ __forceinline__ double tab_kernel(int m, int k) const { return __ldg(&A->models.kernel[ti(m, k)]); }
+  __device__ __forceinline__ double tab_cmp(int m, int k) const { return __ldg(&A->models.self_cmp[ti(m, k)]); }
+  __device__ __forceinline__ double tab_mem(int m, int k) const { return __ldg(&A->models.self_mem[ti(m, k)]); }
+  __device__ __forceinline__ int mprio(int m) const { return __ldg(&A->models.prio[m]); }
+  __device__ __forceinline__ double mdeadline(int m) const { return __ldg(&A->models.deadline[m]); }
+  __device__ __forceinline__ double mtimeout(int m) const { return __ldg(&A->models.timeout[m]); }
+  __device__ __forceinline__ int mmaxb(int m) const { return __ldg(&A->models.max_batch[m]); }
+  __device__ __forceinline__ int64_t req_at(int pos) const { return __ldg(&A->model_req[pos]); }
+  __device__ __forceinline__ double arr(int64_t gidx) const { return __ldg(&A->arr_time[gidx]); }
+  __device__ __forceinline__ int q_len(int m) const { return QI(QI_TAIL, m) - QI(QI_HEAD, m); }
+  __device__ __forceinline__ double front_arrival(int m) const { return arr(req_at(QI(QI_HEAD, m))); }
+
+  __device__ __forceinline__ void push_event(int i, double t, int kind) {  // Simulation._push (simulation.py:202-205)
+    ++seq;
+    put(ed[i], t);
+    put(ek[i], ((unsigned long long)kind << 56) | seq);
+  }
+  __device__ __forceinline__ void clear_event(int i) {
+    put(ed[i], __longlong_as_double(0x7ff0000000000000LL));
+    put(ek[i], kNoKey);
+  }
+
+  __device__ __forceinline__ void cap_row_at(int64_t n, double t, int g, double pct) const {
+    if (n < A->cap_rows_max) {
+      const int64_t o = r * A->cap_rows_max + n;
+      A->cap_time[o] = t;
+      A->cap_gpu[o] = (int16_t)g;
+      A->cap_pct[o] = pct;
+    }
+  }
+
+  // ------------------------------------------------------------ timelines (domain.py:237-264)
+  // lane-local: called by the one lane that owns slot s
+  __device__ __forceinline__ bool tl_record(int s, double now, const double (&v)[NM]) const {
+    if (SB(SB_TLEN, s)) {
+      const double last = SD(SD_TL, s);
+      if (now < last) return false;  // SimulationOrderError
+      if (now == last) {             // same timestamp: replace the last sample
+#pragma unroll
+        for (int i = 0; i < NM; ++i) SD(SD_VL + i, s) = v[i];
+        return true;
+      }
+      const double d = now - last;  // closes segment [last, now) of the held value
+#pragma unroll
+      for (int i = 0; i < NM; ++i) SD(SD_ACC + i, s) = SD(SD_ACC + i, s) + SD(SD_VL + i, s) * d;
+      SD(SD_TL, s) = now;
+#pragma unroll
+      for (int i = 0; i < NM; ++i) SD(SD_VL + i, s) = v[i];
+      return true;
+    }
+    SB(SB_TLEN, s) = 1;
+    SD(SD_T0, s) = now;
+    SD(SD_TL, s) = now;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) {
+      SD(SD_VL + i, s) = v[i];
+      SD(SD_ACC + i, s) = 0.0;
+    }
+    return true;
+  }
+  __device__ __forceinline__ void tl_twa(int s, double end, double (&out)[NM]) const {
+    const double total = end - SD(SD_T0, s);
+    if (total <= 0.0) {
+#pragma unroll
+      for (int i = 0; i < NM; ++i) out[i] = SD(SD_VL + i, s);
+      return;
+    }
+    const double d = end - SD(SD_TL, s);
+#pragma unroll
+    for (int i = 0; i < NM; ++i) out[i] = (SD(SD_ACC + i, s) + SD(SD_VL + i, s) * d) / total;
+  }
+
+  // ------------------------------------------------------------ runtime (runtime.py:104-141)
+  // aggregate = sum of contributions in running-list order from 0.0; lane i owns metric i
+  __device__ __forceinline__ void recompute_aggregate(int g) {
+    if (lane < NM) {
+      double a = 0.0;
+      const int n = GI(GI_NRUN, g);
+      for (int p = 0; p < n; ++p) {
+        const int s = slot_at(g, p);
+        a += thr(SB(SB_MODEL, s), SB(SB_SIZE, s), lane);
+      }
+      GD(GD_AGG + lane, g) = a;
+    }
+    sync();
+  }
+  // every running entry records aggregate_excluding(self) at now; lane p owns list position p
+  __device__ __forceinline__ void stamp_all(int g, double now) {
+    bool bad = false;
+    if (lane < GI(GI_NRUN, g)) {
+      const int s = slot_at(g, lane);
+      const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s);
+      double v[NM];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) v[i] = GD(GD_AGG + i, g) - thr(m, k, i);
+      bad = !tl_record(s, now, v);
+      SI(SI_ICP, s) = -1;  // the cached intf_cur of this entry is stale now
+    }
+    sync();
+    fail_any(bad, STRAIT_EORDER);
+  }
+
+  // ------------------------------------------------------------ ground truth (oracle.py:55-77)
+  __device__ __forceinline__ double gt_slowdown(int g, int s) const {
+    const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s);
+    const double cmp = tab_cmp(m, k), mem = tab_mem(m, k);
+    double x = cf->gt_w_cmp * cmp + cf->gt_w_mem * mem;
+#pragma unroll
+    for (int i = 0; i < NM; ++i) x += cf->gt_w[i] * (GD(GD_AGG + i, g) - thr(m, k, i));
+    double effect = cf->gt_family == 0 ? cf->gt_scale * pow(cf->gt_base, x) + cf->gt_offset
+                                       : cf->gt_scale * x * x + cf->gt_offset;
+    effect = py_max(0.0, effect);
+    return 1.0 + effect * (SB(SB_PRIO, s) == 0 ? cf->gt_pf_high : cf->gt_pf_low) * SD(SD_NOISE, s);
+  }
+
+  // ExecutionState.advance (simulation.py:54-70); lane-local
+  __device__ __forceinline__ bool ex_consume(int s, double now) const {
+    const double d = now - SD(SD_LAST, s);
+    bool ok = !(d < 0);
+    if (d > 0) {
+      const double slow = SD(SD_SLOW, s);
+      SD(SD_WORK, s) = SD(SD_WORK, s) + d / slow;
+      double rem = SD(SD_REM, s) - d / slow;
+      if (rem < -kWorkEps) ok = false;
+      if (rem < 0.0) rem = 0.0;
+      SD(SD_REM, s) = rem;
+    }
+    SD(SD_LAST, s) = now;
+    return ok;
+  }
+
+  // Simulation._recompute (simulation.py:290-297): every STARTED entry of GPU g
+  // integrates its work so far, takes the new ground-truth slowdown and
+  // re-pushes its kernel-complete (fresh seq, list order).  Lane p = position p.
+  __device__ __forceinline__ void recompute(int g, double now) {
+    const int n = GI(GI_NRUN, g);
+    int s = -1;
+    bool started = false, ok = true;
+    double eta = 0.0;
+    if (lane < n) {
+      s = slot_at(g, lane);
+      started = SB(SB_STARTED, s);
+      if (started) {
+        ok = ex_consume(s, now);
+        const double slow = gt_slowdown(g, s);
+        SD(SD_SLOW, s) = slow;
+        eta = SD(SD_LAST, s) + SD(SD_REM, s) * slow;
+      }
+    }
+    const unsigned mask = __ballot_sync(kFull, started);
+    if (started) {
+      const unsigned long long q = seq + 1 + __popc(mask & ((1u << lane) - 1));
+      ed[s] = eta;
+      ek[s] = ((unsigned long long)kKC << 56) | q;
+    }
+    seq += __popc(mask);
+    sync();
+    fail_any(!ok, STRAIT_EORDER);
+  }
+
+  // _signal_hp_violation (simulation.py:223-229) -> AimdState.reset (runtime.py:36-37)
+  __device__ __forceinline__ void signal_hp(int gpu_id, double now) {
+    for (int g0 = 0; g0 < NG; g0 += 32) {
+      const int g = g0 + lane;
+      bool changed = false;
+      double cap = 0.0;
+      if (g < NG && (gpu_id < 0 || g == gpu_id)) {
+        const double old = GD(GD_CAP, g);
+        cap = cf->aimd_floor;
+        GD(GD_CAP, g) = cap;
+        changed = cap != old;
+      }
+      const unsigned mask = __ballot_sync(kFull, changed);
+      if (changed) cap_row_at(c_cap_rows + __popc(mask & ((1u << lane) - 1)), now, g, cap);
+      c_cap_rows += __popc(mask);
+    }
+    sync();
+  }
+
+  // ------------------------------------------------------------ predictor (predictor.py)
+  // InterferencePredictor.update (predictor.py:345-363) for one sample, all lanes;
+  // lane k owns parameter k and its Adam moments.
+  __device__ __forceinline__ void update(const double (&tw)[NM], double cmp, double mem, int prio, double actual,
+                                         double& predicted, double& residual, bool& skipped, bool& saturated) {
+    const bool owner = lane < NP;
+    const double cap = pr.cap;
+    const double x = pr.exponent(tw, cmp, mem);
+    const double z = x * pr.log_base;
+    double inner, pow_bx = 0.0;
+    if (z > kLogSaturate) {
+      saturated = true;
+      inner = __longlong_as_double(0x7ff0000000000000LL);
+    } else {
+      pow_bx = exp(z);
+      inner = pr.scale * pow_bx + pr.offset;
+      saturated = inner >= cap;
+    }
+    const double eff = saturated ? cap : py_min(py_max(inner, 0.0), cap);
+    const int own = NM + (prio == 0 ? 5 : 6), other = NM + (prio == 0 ? 6 : 5);
+    const double cfc = prio == 0 ? pr.coeff[0] : pr.coeff[1];
+    predicted = 1.0 + eff * cfc;
+    double d = 0.0;
+    const bool clamp_active = saturated || inner <= 0.0 || inner >= cap;
+    if (!clamp_active && owner) {  // _prediction_gradient (predictor.py:285-299)
+      const double log_b = pr.log_base;
+      const double zz = pr.scale * pow_bx;
+      if (lane == 0) d = pow_bx * cfc;
+      else if (lane == 1) d = pr.scale * x * exp((x - 1.0) * log_b) * cfc;
+      else if (lane == 2) d = cfc;
+      else if (lane < 3 + NM) {
+        double ai = 0.0;
+#pragma unroll
+        for (int k = 0; k < NM; ++k)
+          if (lane == 3 + k) ai = tw[k];
+        d = zz * log_b * ai * cfc;
+      } else if (lane == 3 + NM) d = zz * log_b * cmp * cfc;
+      else if (lane == 4 + NM) d = zz * log_b * mem * cfc;
+    }
+    if (lane == own) d = eff;
+    residual = predicted - actual;
+    const double delta = cf->huber_delta;  // huber_grad (predictor.py:155-158)
+    const double gh = fabs(residual) <= delta ? residual : (residual > 0 ? delta : -delta);
+    const double gk = gh * d;
+    const bool finite = __all_sync(kFull, !owner || isfinite(gk)) && isfinite(residual);
+    skipped = !finite;
+    if (!finite) return;  // UpdateResult(skipped=True)
+    ++step;               // adam_step (predictor.py:124-145)
+    const double bc1 = step <= A->n_bc ? __ldg(&A->bc1[step - 1]) : 1.0;
+    const double bc2 = step <= A->n_bc ? __ldg(&A->bc2[step - 1]) : 1.0;
+    const double b1 = cf->beta1, b2 = cf->beta2;
+    double p = owner ? P[lane] : 0.0;
+    if (owner && lane != other) {
+      adam_m = b1 * adam_m + (1.0 - b1) * gk;
+      adam_v = b2 * adam_v + (1.0 - b2) * gk * gk;
+      const double m_hat = adam_m / bc1;
+      const double v_hat = adam_v / bc2;
+      p -= cf->learning_rate * m_hat / (sqrt(v_hat) + cf->eps);
+      if (lane == 0) p = py_max(p, 1e-6);        // enforce_floors (predictor.py:98-102)
+      if (lane == 1) p = py_max(p, 1.0 + 1e-6);
+    }
+    if (lane == NM + 5 || lane == NM + 6) p = py_max(p, 1e-6);
+    sync();
+    if (owner) P[lane] = p;
+    sync();
+    pr.load(P, cap);
+  }
+
+  // ------------------------------------------------------------ dispatch (scheduler.py)
+  // check_violate (scheduler.py:118-161) of candidate (m, k) on GPU g; lane-local.
+  __device__ __forceinline__ bool violate(int g, int m, int k, int cprio, double now, int pass_id) const {
+    const int n = GI(GI_NRUN, g);
+    if (cprio == 1) {  // LOW: LP aggregate + contribution vs the AIMD cap (runtime.py:116-122)
+      const double capf = GD(GD_CAP, g) / 100.0;
+      double lp[NM];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) lp[i] = 0.0;
+      for (int p = 0; p < n; ++p) {
+        const int s = slot_at(g, p);
+        if (SB(SB_PRIO, s) == 1) {
+          const int em = SB(SB_MODEL, s), ek_ = SB(SB_SIZE, s);
+#pragma unroll
+          for (int i = 0; i < NM; ++i) lp[i] += thr(em, ek_, i);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NM; ++i)
+        if (lp[i] + thr(m, k, i) > capf) return true;
+    }
+    for (int p = 0; p < n; ++p) {
+      const int s = slot_at(g, p);
+      const int ep = SB(SB_PRIO, s);
+      if (ep > cprio) continue;
+      const int em = SB(SB_MODEL, s), ek_ = SB(SB_SIZE, s);
+      double nagg[NM];
+#pragma unroll
+      for (int i = 0; i < NM; ++i) nagg[i] = GD(GD_AGG + i, g) - thr(em, ek_, i) + thr(m, k, i);
+      const double cmp = tab_cmp(em, ek_), mem = tab_mem(em, ek_);
+      const double intf_new = pr.predict(nagg, cmp, mem, ep);
+      const double ks = SD(SD_KS, s);
+      double intf_cur;
+      if (SI(SI_ICP, s) == pass_id) {
+        intf_cur = SD(SD_ICUR, s);
+      } else {  // a function of (entry timeline, now, params) only: cached for the pass
+        double tw[NM];
+        tl_twa(s, now, tw);
+        intf_cur = pr.predict(tw, cmp, mem, ep);
+        SD(SD_ICUR, s) = intf_cur;
+        SI(SI_ICP, s) = pass_id;
+      }
+      const double tk = tab_kernel(em, ek_);
+      const double elapsed = py_max(0.0, now - ks);
+      const double denom = intf_cur * tk;
+      const double progress = denom > 0 ? py_min(1.0, elapsed / denom) : 1.0;
+      const double remaining = (1.0 - progress) * tk * intf_new;
+      const double projected = py_max(now, ks) + remaining;
+      if (projected > SD(SD_DL, s)) return true;
+    }
+    return false;
+  }
+
+  struct Plan {
+    bool ok;
+    int gpu;
+    double lat, intf;
+  };
+
+  // best_for(k) (scheduler.py:263-280): lane per GPU, then the lexicographic
+  // (latency, gpu_id) argmin across lanes.
+  __device__ __forceinline__ Plan best_for(int m, int k, double front, double now, int pass_id) {
+    const int cprio = mprio(m);
+    const double cmp = tab_cmp(m, k), mem = tab_mem(m, k), total = tab_total(m, k), kern = tab_kernel(m, k);
+    const double dl = mdeadline(m);
+    const bool use_violate = cf->use_violate, use_meet = cf->use_meet;
+    bool found = false;
+    int bg = 0x7fffffff;
+    double bl = 0.0, bi = 0.0;
+    for (int g = lane; g < NG; g += 32) {
+      if (!(GI(GI_NRUN, g) < CONC)) continue;  // has_slot (runtime.py:101-102)
+      if (use_violate && violate(g, m, k, cprio, now, pass_id)) continue;
+      double assumed[NM];  // check_meet (scheduler.py:164-185)
+#pragma unroll
+      for (int i = 0; i < NM; ++i) assumed[i] = 0.5 * GD(GD_AGG + i, g);
+      const double intf = pr.predict(assumed, cmp, mem, cprio);
+      const double lat = total + py_max(0.0, GD(GD_TAV, g) - now) + (intf - 1.0) * kern + (now - front);
+      if (use_meet && !(lat <= dl)) continue;
+      if (!found || lat < bl) {
+        found = true;
+        bg = g;
+        bl = lat;
+        bi = intf;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const bool f2 = __shfl_xor_sync(kFull, found, off);
+      const int g2 = __shfl_xor_sync(kFull, bg, off);
+      const double l2 = __shfl_xor_sync(kFull, bl, off);
+      const double i2 = __shfl_xor_sync(kFull, bi, off);
+      if (f2 && (!found || l2 < bl || (l2 == bl && g2 < bg))) {
+        found = true;
+        bg = g2;
+        bl = l2;
+        bi = i2;
+      }
+    }
+    sync();  // intf_cur cache writes
+    return Plan{found, bg, bl, bi};
+  }
+
+  // PredictivePolicy.propose (scheduler.py:257-285) + largest_feasible (:78-90).
+  // Probes never repeat, so the memo reduces to the plan of the last feasible probe.
+  __device__ __forceinline__ int propose(int m, double now, int pass_id, Plan& plan) {
+    const double front = front_arrival(m);
+    const int kmax = min(q_len(m), mmaxb(m));
+    int lo = 1, hi = kmax, bestk = 0;
+    while (lo <= hi) {
+      const int mid = (lo + hi) / 2;
+      const Plan p = best_for(m, mid, front, now, pass_id);
+      if (p.ok) {
+        bestk = mid;
+        plan = p;
+        lo = mid + 1;
+      } else {
+        hi = mid - 1;
+      }
+    }
+    return bestk;
+  }
+
+  // early_drop (scheduler.py:65-75).  deadline_abs - now is monotone in queue
+  // order (FIFO of nondecreasing arrival times plus a per-model deadline_ms, and
+  // rounding is monotone), so the dropped set is always a prefix of the queue.
+  __device__ __forceinline__ void early_drop(int m, double now) {
+    const int h = QI(QI_HEAD, m), t = QI(QI_TAIL, m);
+    if (h == t) return;
+    const double floor_latency = tab_total(m, 1), dl = mdeadline(m);
+    int ndrop = 0;
+    for (int b = h; b < t; b += 32) {
+      const int p = b + lane;
+      const bool drop = p < t && (arr(req_at(p)) + dl) - now < floor_latency;
+      const unsigned mask = __ballot_sync(kFull, drop);
+      if (mask == kFull) {
+        ndrop += 32;
+        continue;
+      }
+      ndrop += __ffs(~mask) - 1;
+      break;
+    }
+    if (!ndrop) return;
+    for (int i = lane; i < ndrop; i += 32) {  // request rows of the dropped (simulation.py:240-257)
+      const int64_t gidx = req_at(h + i);
+      A->req_status[gidx] = 2;
+      A->req_violated[gidx] = 1;
+      A->req_completion[gidx] = __longlong_as_double(0x7ff8000000000000LL);
+      A->req_batch[gidx] = -1;
+    }
+    resolved += ndrop;
+    if (mprio(m) == 0) c_hp_drop += ndrop, c_hp_viol += ndrop;
+    else c_lp_drop += ndrop, c_lp_viol += ndrop;
+    put(QI(QI_HEAD, m), h + ndrop);
+    put(QI(QI_FGEN, m), QI(QI_FGEN, m) + 1);
+    sync();
+    if (mprio(m) == 0) signal_hp(-1, now);  // simulation.py:352-357
+  }
+
+  // submit_plan (scheduler.py:295-324) + Simulation on_submit (simulation.py:305-350)
+  __device__ __forceinline__ void submit(int m, int k, const Plan& plan, double now, int pass_id) {
+    const int bid = batch_seq++;
+    const int g = plan.gpu;
+    const int h = QI(QI_HEAD, m);
+    const int n = GI(GI_NRUN, g);
+    int j = 0;
+    while (j < C && SB(SB_LIVE, slot(g, j))) ++j;
+    if (j >= C || n >= CONC) {  // GpuRuntimeState.add_entry (runtime.py:125-126)
+      fail(STRAIT_ERUNTIME);
+      return;
+    }
+    const int s = slot(g, j);
+    const double d = tab_transfer(m, k);
+    if (!(d > 0)) fail(STRAIT_EINVAL);  // PcieLinkState.reserve (pcie.py:28-29)
+    const double start = py_max(now, GD(GD_TAV, g)), end = start + d;
+    const double front = arr(req_at(h));
+    const double noise = cf->has_noise ? __ldg(&A->noise[base + bid]) : 1.0;  // simulation.py:309-311
+    if (lane == 0) {
+      QI(QI_HEAD, m) = h + k;  // TaskQueue.pop_front
+      QI(QI_FGEN, m) = QI(QI_FGEN, m) + 1;
+      GD(GD_TAV, g) = end;
+      GD(GD_PEND + (GI(GI_PHEAD, g) + GI(GI_PN, g)) % C, g) = end;
+      GI(GI_PN, g) = GI(GI_PN, g) + 1;
+      SB(SB_MODEL, s) = (int8_t)m;
+      SB(SB_SIZE, s) = (int8_t)k;
+      SB(SB_PRIO, s) = (int8_t)mprio(m);
+      SB(SB_STARTED, s) = 0;
+      SB(SB_LIVE, s) = 1;
+      SB(SB_TLEN, s) = 0;
+      SI(SI_BID, s) = bid;
+      SI(SI_REQ0, s) = h;
+      SI(SI_ICP, s) = -1;
+      SD(SD_DL, s) = front + mdeadline(m);
+      SD(SD_KS, s) = end;  // kernel_start_estimate
+      SD(SD_REM, s) = tab_kernel(m, k);
+      SD(SD_SLOW, s) = 1.0;
+      SD(SD_NOISE, s) = noise;
+      SD(SD_LAST, s) = 0.0;
+      SD(SD_WORK, s) = 0.0;
+      ORD(n, g) = (int8_t)j;
+      GI(GI_NRUN, g) = n + 1;
+    }
+    sync();
+    recompute_aggregate(g);
+    stamp_all(g, now);
+    push_event(s, end, kTC);
+    sync();
+    recompute(g, now);
+    if (lane == 0) {
+      const int64_t o = base + bid;
+      A->dec_time[o] = now;
+      A->dec_pass[o] = pass_id;
+      A->dec_model[o] = (int16_t)m;
+      A->dec_size[o] = (int8_t)k;
+      A->dec_gpu[o] = (int16_t)g;
+      A->dec_est_latency[o] = plan.lat;
+      A->dec_intf[o] = plan.intf;
+      A->b_front[o] = front;
+      A->b_transfer_start[o] = start;
+      A->b_transfer_end[o] = end;
+    }
+    ++c_batches;
+  }
+
+  // _ensure_timeout for one model (simulation.py:231-238)
+  __device__ __forceinline__ void ensure_timeout(int m, double now) {
+    if (!q_len(m) || QI(QI_TGEN, m) == QI(QI_FGEN, m)) return;
+    const double t = py_max(now, front_arrival(m) + mtimeout(m));
+    const int gen = QI(QI_FGEN, m);
+    push_event(S + m, t, kTO);
+    put(QI(QI_EGEN, m), gen);
+    put(QI(QI_TGEN, m), gen);
+    sync();
+  }
+
+  // Simulation._pass (simulation.py:301-361) + run_scheduling_pass (scheduler.py:355-378)
+  __device__ __forceinline__ void do_pass(double now) {
+    const int pass_id = ++pass_seq;
+    ++c_passes;
+    // queue_order (scheduler.py:249-255): stable sort of the ready queues by
+    // (priority, front arrival, model_id), as a lane-parallel rank sort.
+    for (int m = lane; m < M; m += 32) {
+      const bool rdy = q_len(m) > 0;
+      qb[m] = rdy;
+      qd[m] = rdy ? front_arrival(m) : 0.0;
+    }
+    sync();
+    const bool use_prio = cf->use_priority_order;
+    int n = 0;
+    for (int m0 = 0; m0 < M; m0 += 32) {
+      const int m = m0 + lane;
+      const bool rdy = m < M && qb[m];
+      if (rdy) {
+        const int pm = use_prio ? mprio(m) : 0;
+        const double fm = qd[m];
+        int rank = 0;
+        for (int j = 0; j < M; ++j) {
+          if (!qb[j] || j == m) continue;
+          const int pj = use_prio ? mprio(j) : 0;
+          const double fj = qd[j];
+          rank += pj != pm ? pj < pm : (fj != fm ? fj < fm : j < m);
+        }
+        QI(QI_ORD, rank) = m;
+      }
+      n += __popc(__ballot_sync(kFull, rdy));
+    }
+    sync();
+    for (int i = 0; i < n && !err; ++i) {
+      const int m = QI(QI_ORD, i);
+      early_drop(m, now);
+      const int len = q_len(m);
+      if (!len) continue;
+      if (!(len >= mmaxb(m) || now >= front_arrival(m) + mtimeout(m))) continue;  // TaskQueue.eligible
+      Plan plan;
+      const int k = propose(m, now, pass_id, plan);
+      if (!k) continue;
+      submit(m, k, plan, now, pass_id);
+    }
+    // _ensure_timeout for every queue in model order (simulation.py:360-361)
+    for (int m0 = 0; m0 < M; m0 += 32) {
+      const int m = m0 + lane;
+      const bool need = m < M && q_len(m) > 0 && QI(QI_TGEN, m) != QI(QI_FGEN, m);
+      const unsigned mask = __ballot_sync(kFull, need);
+      if (need) {
+        const unsigned long long q = seq + 1 + __popc(mask & ((1u << lane) - 1));
+        ed[S + m] = py_max(now, front_arrival(m) + mtimeout(m));
+        ek[S + m] = ((unsigned long long)kTO << 56) | q;
+        QI(QI_EGEN, m) = QI(QI_FGEN, m);
+        QI(QI_TGEN, m) = QI(QI_FGEN, m);
+      }
+      seq += __popc(mask);
+    }
+    sync();
+  }
+
+  // ------------------------------------------------------------ event handlers
+  __device__ __forceinline__ void on_transfer_complete(int s, double now) {  // simulation.py:378-394
+    const int g = s % G;
+    const int pn = GI(GI_PN, g);
+    if (pn <= 0) {  // PcieLinkState.calibrate with nothing pending (pcie.py:43-44)
+      fail(STRAIT_EINVAL);
+      return;
+    }
+    if (lane == 0) {
+      // calibrate (pcie.py:36-53): FIFO => the oldest reservation is this batch's
+      const int ph = GI(GI_PHEAD, g);
+      const double predicted = GD(GD_PEND + ph, g);
+      const int nph = (ph + 1) % C, npn = pn - 1;
+      GI(GI_PHEAD, g) = nph;
+      GI(GI_PN, g) = npn;
+      if (!npn) {
+        GD(GD_TAV, g) = now;
+      } else {
+        const double off = now - predicted;
+        if (off != 0.0) {
+          GD(GD_TAV, g) = GD(GD_TAV, g) + off;
+          for (int i = 0; i < npn; ++i) GD(GD_PEND + (nph + i) % C, g) = GD(GD_PEND + (nph + i) % C, g) + off;
+        }
+      }
+      SB(SB_STARTED, s) = 1;
+      SD(SD_KS, s) = now;  // kernel_start (and kernel_start_estimate)
+      SB(SB_TLEN, s) = 0;  // timeline reset to the kernel window
+      double v[NM];
+      const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s);
+#pragma unroll
+      for (int i = 0; i < NM; ++i) v[i] = GD(GD_AGG + i, g) - thr(m, k, i);
+      tl_record(s, now, v);
+      SI(SI_ICP, s) = -1;
+      SD(SD_SLOW, s) = gt_slowdown(g, s);
+      SD(SD_LAST, s) = now;
+      A->b_kernel_start[base + SI(SI_BID, s)] = now;
+    }
+    sync();
+    push_event(s, SD(SD_LAST, s) + SD(SD_REM, s) * SD(SD_SLOW, s), kKC);
+    sync();
+  }
+
+  // simulation.py:396-460 (+ complete_batch, scheduler.py:327-352)
+  __device__ __forceinline__ void on_kernel_complete(int s, double now) {
+    const int g = s % G;
+    const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s), prio = SB(SB_PRIO, s);
+    const int bid = SI(SI_BID, s), req0 = SI(SI_REQ0, s);
+    bool ok = true;
+    if (lane == 0) ok = ex_consume(s, now);
+    fail_any(!ok, STRAIT_EORDER);
+    sync();
+    const double measured = now - SD(SD_KS, s);
+    const double completion = now + (tab_total(m, k) - tab_transfer(m, k) - tab_kernel(m, k));
+    const double dl = mdeadline(m);
+    int nviol = 0;
+    for (int i0 = 0; i0 < k; i0 += 32) {
+      const int i = i0 + lane;
+      bool viol = false;
+      if (i < k) {
+        const int64_t gidx = req_at(req0 + i);
+        viol = completion > arr(gidx) + dl;
+        A->req_status[gidx] = 1;
+        A->req_violated[gidx] = (uint8_t)viol;
+        A->req_completion[gidx] = completion;
+        A->req_batch[gidx] = bid;
+      }
+      nviol += __popc(__ballot_sync(kFull, viol));
+    }
+    resolved += k;
+    if (prio == 0) c_hp_viol += nviol;
+    else c_lp_viol += nviol;
+    double tw[NM];
+    tl_twa(s, now, tw);
+    const double tk = tab_kernel(m, k);
+    const double actual = measured / tk;
+    if (!(actual > 0)) fail(STRAIT_EINVAL);
+    // GpuRuntimeState.remove_entry (runtime.py:132-141): shift the running list
+    const int n = GI(GI_NRUN, g);
+    const int j = s / G;
+    int pos = 0;
+    while (pos < n && ORD(pos, g) != j) ++pos;
+    if (pos == n) fail(STRAIT_ERUNTIME);
+    const double work = SD(SD_WORK, s);
+    sync();
+    if (lane == 0) {
+      for (int p = pos; p + 1 < n; ++p) ORD(p, g) = ORD(p + 1, g);
+      GI(GI_NRUN, g) = n - 1;
+      SB(SB_LIVE, s) = 0;
+    }
+    clear_event(s);
+    sync();
+    recompute_aggregate(g);
+    stamp_all(g, now);
+    double predicted, residual;
+    bool skipped, saturated;
+    update(tw, tab_cmp(m, k), tab_mem(m, k), prio, actual, predicted, residual, skipped, saturated);
+    if (lane == 0) {
+      const int64_t o = base + bid;
+      A->fb_predicted[o] = predicted;
+      A->fb_actual[o] = actual;
+      A->fb_residual[o] = residual;
+      A->fb_flags[o] = (uint8_t)((skipped ? 1 : 0) | (saturated ? 2 : 0));
+      A->b_kernel_end[o] = now;
+      A->b_completion[o] = completion;
+      A->b_work[o] = work;
+      A->b_done_order[o] = done_order;
+    }
+    ++done_order;
+    ++c_completed;
+    recompute(g, now);
+    if (prio == 0 && nviol) signal_hp(g, now);  // simulation.py:458-459
+  }
+
+  __device__ __forceinline__ void on_tick_advance(double now) {  // AimdState.advance (runtime.py:26-34)
+    bool bad = false;
+    for (int g0 = 0; g0 < NG; g0 += 32) {
+      const int g = g0 + lane;
+      bool changed = false;
+      double cap = 0.0;
+      if (g < NG) {
+        const double old = GD(GD_CAP, g), last = GD(GD_TICK, g);
+        if (now < last) bad = true;
+        const double whole = floor((now - last) / cf->aimd_interval);
+        cap = old;
+        if (whole > 0) {
+          cap = py_min(cf->aimd_ceiling, old + whole * cf->aimd_increase);
+          GD(GD_CAP, g) = cap;
+          GD(GD_TICK, g) = last + whole * cf->aimd_interval;
+        }
+        changed = cap != old;
+      }
+      const unsigned mask = __ballot_sync(kFull, changed);
+      if (changed) cap_row_at(c_cap_rows + __popc(mask & ((1u << lane) - 1)), now, g, cap);
+      c_cap_rows += __popc(mask);
+    }
+    sync();
+    fail_any(bad, STRAIT_EINVAL);
+  }
+
+  // ------------------------------------------------------------ main loop (simulation.py:475-513)
+  __device__ __forceinline__ void run() {
+    const double INF = __longlong_as_double(0x7ff0000000000000LL);
+    const int np = NP;
+    const double* st = A->pred_state + r * 3 * np;
+    if (lane < np) P[lane] = st[lane];
+    adam_m = lane < np ? st[np + lane] : 0.0;
+    adam_v = lane < np ? st[2 * np + lane] : 0.0;
+    step = A->pred_step[r];
+    for (int g = lane; g < G; g += 32) {
+      GD(GD_TAV, g) = 0.0;
+      GD(GD_CAP, g) = cf->aimd_floor;
+      GD(GD_TICK, g) = 0.0;
+      GI(GI_NRUN, g) = 0;
+      GI(GI_PHEAD, g) = 0;
+      GI(GI_PN, g) = 0;
+#pragma unroll
+      for (int i = 0; i < NM; ++i) GD(GD_AGG + i, g) = 0.0;
+    }
+    for (int s = lane; s < S; s += 32) {
+      SB(SB_LIVE, s) = 0;
+      SI(SI_ICP, s) = -1;
+    }
+    for (int i = lane; i < NE; i += 32) {
+      ed[i] = INF;
+      ek[i] = kNoKey;
+    }
+    int64_t hp_arr = 0, lp_arr = 0;
+    for (int m = lane; m < M; m += 32) {
+      const int64_t b = A->mr_off[r * M + m], e = A->mr_off[r * M + m + 1];
+      QI(QI_HEAD, m) = QI(QI_TAIL, m) = (int)b;
+      QI(QI_FGEN, m) = 0;
+      QI(QI_TGEN, m) = -1;
+      QI(QI_EGEN, m) = 0;
+      if (mprio(m) == 0) hp_arr += e - b;
+      else lp_arr += e - b;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      hp_arr += __shfl_xor_sync(kFull, hp_arr, off);
+      lp_arr += __shfl_xor_sync(kFull, lp_arr, off);
+    }
+    for (int64_t i = lane; i < N; i += 32) A->req_status[base + i] = 0;
+    for (int g = lane; g < NG; g += 32) cap_row_at(g, 0.0, g, cf->aimd_floor);  // simulation.py:196-197
+    sync();
+    pr.load(P, cf->effect_cap);
+    c_cap_rows = NG;
+    seq = (unsigned long long)N;  // the arrivals took seq 1..N (simulation.py:184-194)
+    next_arr = 0;
+    if (N) {
+      push_event(S + M, cf->aimd_interval, kTICK);
+      put(ed[S + M + 1], arr(base));
+      put(ek[S + M + 1], (unsigned long long)kARR << 56);
+    }
+    sync();
+
+    while (!err) {
+      // next event: lexicographic argmin of (time, kind << 56 | seq) over all homes
+      double bt = INF;
+      unsigned long long bk = kNoKey;
+      int bi = -1;
+      for (int i = lane; i < NE; i += 32) {
+        const double t = ed[i];
+        const unsigned long long kk = ek[i];
+        if (t < bt || (t == bt && kk < bk)) bt = t, bk = kk, bi = i;
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        const double t2 = __shfl_xor_sync(kFull, bt, off);
+        const unsigned long long k2 = __shfl_xor_sync(kFull, bk, off);
+        const int i2 = __shfl_xor_sync(kFull, bi, off);
+        if (t2 < bt || (t2 == bt && k2 < bk)) bt = t2, bk = k2, bi = i2;
+      }
+      if (bk == kNoKey) break;
+      const int kind = (int)(bk >> 56);
+      const double now = bt;
+      ++c_events;
+      // each handler's pre-pass part, at most one pass, then the post-pass part,
+      // so the pass is instantiated once
+      bool pass = false;
+      int post_timeout = -1;
+      bool post_tick = false;
+      if (kind == kARR) {  // _on_arrival (simulation.py:365-371)
+        const int64_t gidx = base + next_arr;
+        ++next_arr;
+        put(ed[S + M + 1], next_arr < N ? arr(base + next_arr) : INF);
+        put(ek[S + M + 1], next_arr < N ? (unsigned long long)kARR << 56 : kNoKey);
+        const int m = __ldg(&A->arr_model[gidx]);
+        const int t = QI(QI_TAIL, m);
+        if (req_at(t) != gidx) fail(STRAIT_EINVAL);  // per-model arrivals must pop in k order
+        put(QI(QI_TAIL, m), t + 1);
+        if (t + 1 - QI(QI_HEAD, m) == 1) put(QI(QI_FGEN, m), QI(QI_FGEN, m) + 1);  // TaskQueue.push
+        sync();
+        pass = q_len(m) == mmaxb(m);
+        post_timeout = m;
+      } else if (kind == kKC) {
+        on_kernel_complete(bi, now);
+        pass = true;
+      } else if (kind == kTC) {
+        on_transfer_complete(bi, now);
+      } else if (kind == kTO) {  // _on_timeout (simulation.py:373-376)
+        const int m = bi - S;
+        const int gen = QI(QI_EGEN, m);
+        clear_event(bi);
+        sync();
+        pass = q_len(m) && gen == QI(QI_FGEN, m);
+      } else {  // _on_tick (simulation.py:462-471)
+        clear_event(bi);
+        sync();
+        on_tick_advance(now);
+        pass = true;
+        post_tick = true;
+      }
+      if (pass && !err) do_pass(now);
+      if (post_timeout >= 0) ensure_timeout(post_timeout, now);
+      if (post_tick && resolved < N) {
+        push_event(S + M, now + cf->aimd_interval, kTICK);
+        sync();
+      }
+    }
+    if (!err && resolved != N) err = STRAIT_EORDER;  // unresolved requests (simulation.py:491-494)
+    sync();
+    double* so = A->pred_state + r * 3 * np;
+    if (lane < np) {
+      so[lane] = P[lane];
+      so[np + lane] = adam_m;
+      so[2 * np + lane] = adam_v;
+    }
+    if (lane == 0) {
+      A->pred_step[r] = step;
+      int64_t* c = A->counters + r * STRAIT_RC_N;
+      for (int i = 0; i < STRAIT_RC_N; ++i) c[i] = 0;
+      c[STRAIT_RC_ERROR] = err;
+      c[STRAIT_RC_BATCHES] = c_batches;
+      c[STRAIT_RC_COMPLETED] = c_completed;
+      c[STRAIT_RC_PASSES] = c_passes;
+      c[STRAIT_RC_CAP_ROWS] = c_cap_rows;
+      c[STRAIT_RC_EVENTS] = c_events;
+      c[STRAIT_RC_HP_ARR] = hp_arr;
+      c[STRAIT_RC_LP_ARR] = lp_arr;
+      c[STRAIT_RC_HP_VIOL] = c_hp_viol;
+      c[STRAIT_RC_LP_VIOL] = c_lp_viol;
+      c[STRAIT_RC_HP_DROP] = c_hp_drop;
+      c[STRAIT_RC_LP_DROP] = c_lp_drop;
+      c[STRAIT_RC_RESOLVED] = resolved;
+    }
+  }
+};
+
+template <int NM>
+__global__ void __launch_bounds__(128) replay_kernel(const __grid_constant__ StraitReplayArgs a, int wpc) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int w = threadIdx.x >> 5;
+  const int64_t r = (int64_t)blockIdx.x * wpc + w;
+  if (r >= a.n_replays) return;
+  const Layout L(a.max_gpus, a.max_concurrency, a.models.n_models, NM);
+  unsigned char* base = smem + (size_t)w * L.bytes;
+  Sim<NM> S;
+  S.A = &a;
+  S.cf = a.cfg + r;
+  S.lane = threadIdx.x & 31;
+  S.r = r;
+  S.G = L.G;
+  S.C = L.C;
+  S.M = L.M;
+  S.S = L.S;
+  S.NE = L.NE;
+  S.B = a.models.stride;
+  S.NG = S.cf->n_gpus;
+  S.CONC = S.cf->concurrency_limit;
+  S.base = a.req_off[r];
+  S.N = a.req_off[r + 1] - S.base;
+  S.P = (double*)(base + L.P);
+  S.sd = (double*)(base + L.sd);
+  S.gd = (double*)(base + L.gd);
+  S.ed = (double*)(base + L.ed);
+  S.ek = (unsigned long long*)(base + L.ek);
+  S.qd = (double*)(base + L.qd);
+  S.si = (int*)(base + L.si);
+  S.gi = (int*)(base + L.gi);
+  S.qi = (int*)(base + L.qi);
+  S.sb = (int8_t*)(base + L.sb);
+  S.go = (int8_t*)(base + L.go);
+  S.qb = (int8_t*)(base + L.qb);
+  S.batch_seq = S.pass_seq = S.done_order = S.err = 0;
+  S.resolved = 0;
+  S.c_batches = S.c_completed = S.c_passes = S.c_events = 0;
+  S.c_hp_viol = S.c_lp_viol = S.c_hp_drop = S.c_lp_drop = 0;
+  S.run();
+}
+
+// host side: launch one instantiation (explicitly specialised in strait_replay_nm*.cu)
+template <int NM>
+int launch_replay(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp);
+
+#define STRAIT_INSTANTIATE_REPLAY(NMV)                                                                      \
+  template <>                                                                                               \
+  int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) {       \
+    const size_t smem = smem_per_warp * wpc;                                                                \
+    if (cudaFuncSetAttribute(replay_kernel<NMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != \
+        cudaSuccess)                                                                                        \
+      return set_error(STRAIT_ECUDA, "strait_replay: cannot reserve %zu B of shared memory", smem);         \
+    const unsigned grid = (unsigned)((a.n_replays + wpc - 1) / wpc);                                        \
+    replay_kernel<NMV><<<grid, 32 * wpc, smem, st>>>(a, wpc);                                               \
+    return check_launch("strait_replay");                                                                   \
+  }
+
+}  // namespace rp
+}  // namespace strait

@@ -187,6 +187,8 @@ class ReplayBatch:
     def args(self, inputs: dict, outputs: dict, ptr) -> ReplayArgs:
         a = ReplayArgs()
         a.n_replays, a.cap_rows_max, a.n_bc = self.R, self.cap_rows_max, len(self.inputs["bc1"])
+        a.max_gpus = max(s.config.n_gpus for s in self.specs)
+        a.max_concurrency = max(s.config.concurrency_limit for s in self.specs)
         t = self.tab
         md = a.models
         md.n_models, md.n_metrics, md.stride = t["M"], t["nm"], t["B"]
