@@ -8,14 +8,21 @@ NVFLAGS := -O3 -lineinfo $(ARCH) --fmad=false -prec-div=true -prec-sqrt=true -ft
            -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -warn-spills
 LIB := paper_2604_28175_b200/_strait.so
 CSRC := $(wildcard paper_2604_28175_b200/csrc/*.cu)
-CHDR := $(wildcard paper_2604_28175_b200/csrc/*.cuh) include/strait.h
 OBJS := $(patsubst paper_2604_28175_b200/csrc/%.cu,build/%.o,$(CSRC))
 
 all: $(LIB)
 
-build/%.o: paper_2604_28175_b200/csrc/%.cu $(CHDR)
+CDIR := paper_2604_28175_b200/csrc
+COMMON_HDR := $(CDIR)/strait_device.cuh $(CDIR)/strait_capi.cuh include/strait.h
+SWEEP_HDR := $(COMMON_HDR) $(CDIR)/strait_ptx.cuh $(CDIR)/strait_refit.cuh
+REPLAY_HDR := $(COMMON_HDR) $(CDIR)/strait_replay_impl.cuh include/strait_replay.h
+
+build/%.o: $(CDIR)/%.cu $(COMMON_HDR)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -dc -o $@ $<
+
+build/strait_sweep.o: $(SWEEP_HDR)
+$(patsubst $(CDIR)/%.cu,build/%.o,$(wildcard $(CDIR)/strait_replay*.cu)): $(REPLAY_HDR)
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(OBJS)

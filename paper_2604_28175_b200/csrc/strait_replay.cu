@@ -5,6 +5,8 @@
 // compile in parallel.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "strait_capi.cuh"
 #include "strait_replay_impl.cuh"
 
@@ -20,6 +22,15 @@ int sm_count() {
 }
 
 }  // namespace
+
+namespace strait {
+namespace rp {
+int replay_occupancy(int64_t n_replays, int wpc) {
+  if (const char* e = getenv("STRAIT_REPLAY_OCC")) return atoi(e) >= 4 ? 4 : 1;
+  return n_replays > (int64_t)sm_count() * 2 * wpc ? 4 : 1;
+}
+}  // namespace rp
+}  // namespace strait
 
 extern "C" int64_t strait_replay_smem_bytes(int32_t n_gpus, int32_t concurrency_limit, int32_t n_models,
                                             int32_t n_metrics) {

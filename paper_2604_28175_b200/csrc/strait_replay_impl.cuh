@@ -56,19 +56,20 @@ __host__ __device__ __forceinline__ size_t al(size_t x) { return (x + 15) & ~(si
 // engine needs only a handful of base pointers.  Slot s = j * G + g is
 // running-batch slot j of GPU g (G, C = the launch's maximum geometry);
 // per-GPU fields are [field][G] so lanes over GPUs touch consecutive words.
-// Slot double fields (SD_*), then NM timeline values and NM integrals:
-enum { SD_DL, SD_KS, SD_T0, SD_TL, SD_REM, SD_SLOW, SD_NOISE, SD_LAST, SD_WORK, SD_ICUR, SD_VL };
-enum { SI_BID, SI_REQ0, SI_ICP, SI_N };
+// Slot double fields (SD_*), then four NM-vectors: timeline value, timeline
+// integral, the entry's contribution and aggregate_excluding(entry):
+enum { SD_DL, SD_KS, SD_T0, SD_TL, SD_REM, SD_SLOW, SD_NOISE, SD_LAST, SD_WORK, SD_ICUR, SD_CMP, SD_MEM, SD_TK, SD_VL };
+enum { SI_BID, SI_REQ0, SI_N };
 enum { SB_MODEL, SB_SIZE, SB_PRIO, SB_STARTED, SB_LIVE, SB_TLEN, SB_N };
-enum { GD_TAV, GD_CAP, GD_TICK, GD_AGG };  // then NM aggregates, then C pending reservations
+enum { GD_TAV, GD_CAP, GD_TICK, GD_AGG };  // then NM aggregates, NM LP aggregates, C pending reservations
 enum { GI_NRUN, GI_PHEAD, GI_PN, GI_N };
 enum { QI_HEAD, QI_TAIL, QI_FGEN, QI_TGEN, QI_EGEN, QI_ORD, QI_N };
 
 struct Layout {
   int G, C, M, NM, S, NE;
   size_t P, sd, gd, ed, ek, qd, si, gi, qi, sb, go, qb, bytes;
-  __host__ __device__ static int sd_fields(int nm) { return SD_VL + 2 * nm; }
-  __host__ __device__ static int gd_fields(int nm, int c) { return GD_AGG + nm + c; }
+  __host__ __device__ static int sd_fields(int nm) { return SD_VL + 4 * nm; }
+  __host__ __device__ static int gd_fields(int nm, int c) { return GD_AGG + 2 * nm + c; }
   __host__ __device__ Layout(int g, int c, int m, int nm) : G(g), C(c), M(m), NM(nm) {
     S = G * C;
     NE = S + M + 2;
@@ -97,8 +98,11 @@ struct Layout {
 template <int NM>
 struct Sim {
   static constexpr int NP = NM + 7;
-  static constexpr int SD_ACC = SD_VL + NM;
-  static constexpr int GD_PEND = GD_AGG + NM;
+  static constexpr int SD_ACC = SD_VL + NM;   // timeline integral
+  static constexpr int SD_CON = SD_VL + 2 * NM;  // entry.contribution (throughput_at(size))
+  static constexpr int SD_AEX = SD_VL + 3 * NM;  // aggregate_excluding(entry) as last stamped
+  static constexpr int GD_LPA = GD_AGG + NM;     // low_priority_aggregate()
+  static constexpr int GD_PEND = GD_AGG + 2 * NM;
   // ---- launch-wide inputs
   const StraitReplayArgs* A;
   const StraitReplayConfig* cf;
@@ -222,16 +226,20 @@ struct Sim {
   }
 
   // ------------------------------------------------------------ runtime (runtime.py:104-141)
-  // aggregate = sum of contributions in running-list order from 0.0; lane i owns metric i
+  // aggregate_throughput and low_priority_aggregate(): sums of contributions in
+  // running-list order from 0.0 (runtime.py:104-109,116-122); lane i owns metric i
   __device__ __forceinline__ void recompute_aggregate(int g) {
     if (lane < NM) {
-      double a = 0.0;
+      double a = 0.0, lp = 0.0;
       const int n = GI(GI_NRUN, g);
       for (int p = 0; p < n; ++p) {
         const int s = slot_at(g, p);
-        a += thr(SB(SB_MODEL, s), SB(SB_SIZE, s), lane);
+        const double c = SD(SD_CON + lane, s);
+        a += c;
+        if (SB(SB_PRIO, s) == 1) lp += c;
       }
       GD(GD_AGG + lane, g) = a;
+      GD(GD_LPA + lane, g) = lp;
     }
     sync();
   }
@@ -240,24 +248,23 @@ struct Sim {
     bool bad = false;
     if (lane < GI(GI_NRUN, g)) {
       const int s = slot_at(g, lane);
-      const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s);
       double v[NM];
 #pragma unroll
-      for (int i = 0; i < NM; ++i) v[i] = GD(GD_AGG + i, g) - thr(m, k, i);
+      for (int i = 0; i < NM; ++i) {
+        v[i] = GD(GD_AGG + i, g) - SD(SD_CON + i, s);  // aggregate_excluding (runtime.py:111-114)
+        SD(SD_AEX + i, s) = v[i];
+      }
       bad = !tl_record(s, now, v);
-      SI(SI_ICP, s) = -1;  // the cached intf_cur of this entry is stale now
     }
     sync();
     fail_any(bad, STRAIT_EORDER);
   }
 
   // ------------------------------------------------------------ ground truth (oracle.py:55-77)
-  __device__ __forceinline__ double gt_slowdown(int g, int s) const {
-    const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s);
-    const double cmp = tab_cmp(m, k), mem = tab_mem(m, k);
-    double x = cf->gt_w_cmp * cmp + cf->gt_w_mem * mem;
+  __device__ __forceinline__ double gt_slowdown(int s) const {
+    double x = cf->gt_w_cmp * SD(SD_CMP, s) + cf->gt_w_mem * SD(SD_MEM, s);
 #pragma unroll
-    for (int i = 0; i < NM; ++i) x += cf->gt_w[i] * (GD(GD_AGG + i, g) - thr(m, k, i));
+    for (int i = 0; i < NM; ++i) x += cf->gt_w[i] * SD(SD_AEX + i, s);
     double effect = cf->gt_family == 0 ? cf->gt_scale * pow(cf->gt_base, x) + cf->gt_offset
                                        : cf->gt_scale * x * x + cf->gt_offset;
     effect = py_max(0.0, effect);
@@ -293,7 +300,7 @@ struct Sim {
       started = SB(SB_STARTED, s);
       if (started) {
         ok = ex_consume(s, now);
-        const double slow = gt_slowdown(g, s);
+        const double slow = gt_slowdown(s);
         SD(SD_SLOW, s) = slow;
         eta = SD(SD_LAST, s) + SD(SD_REM, s) * slow;
       }
@@ -397,48 +404,58 @@ struct Sim {
   }
 
   // ------------------------------------------------------------ dispatch (scheduler.py)
-  // check_violate (scheduler.py:118-161) of candidate (m, k) on GPU g; lane-local.
-  __device__ __forceinline__ bool violate(int g, int m, int k, int cprio, double now, int pass_id) const {
-    const int n = GI(GI_NRUN, g);
-    if (cprio == 1) {  // LOW: LP aggregate + contribution vs the AIMD cap (runtime.py:116-122)
+  // intf_cur of every running entry = predict(timeline TWA at now) under the
+  // current params (scheduler.py:150-153): a function of (entry timeline, now,
+  // params) only, so it is evaluated once per pass (lane per slot) and
+  // re-evaluated for a GPU's entries after a submission stamps their timelines.
+  __device__ __forceinline__ void icur_slot(int s, double now) const {
+    double tw[NM];
+    tl_twa(s, now, tw);
+    SD(SD_ICUR, s) = pr.predict(tw, SD(SD_CMP, s), SD(SD_MEM, s), SB(SB_PRIO, s));
+  }
+  __device__ __forceinline__ void icur_all(double now) const {
+    for (int s = lane; s < S; s += 32)
+      if (SB(SB_LIVE, s)) icur_slot(s, now);
+    __syncwarp();
+  }
+  __device__ __forceinline__ void icur_gpu(int g, double now) const {
+    if (lane < GI(GI_NRUN, g)) icur_slot(slot_at(g, lane), now);
+    __syncwarp();
+  }
+
+  // the candidate batch (model m at size k): profile row at k (domain.py:52-105)
+  struct Cand {
+    double c[NM];
+    double cmp, mem, total, kern;
+  };
+  __device__ __forceinline__ void load_cand(int m, int k, Cand& cd) const {
+#pragma unroll
+    for (int i = 0; i < NM; ++i) cd.c[i] = thr(m, k, i);
+    cd.cmp = tab_cmp(m, k);
+    cd.mem = tab_mem(m, k);
+    cd.total = tab_total(m, k);
+    cd.kern = tab_kernel(m, k);
+  }
+
+  // check_violate (scheduler.py:118-161) of the candidate on GPU g; lane-local.
+  __device__ __forceinline__ bool violate(int g, const Cand& cd, int cprio, double now) const {
+    if (cprio == 1) {  // LOW: LP aggregate + contribution vs the AIMD cap (:130-135)
       const double capf = GD(GD_CAP, g) / 100.0;
-      double lp[NM];
-#pragma unroll
-      for (int i = 0; i < NM; ++i) lp[i] = 0.0;
-      for (int p = 0; p < n; ++p) {
-        const int s = slot_at(g, p);
-        if (SB(SB_PRIO, s) == 1) {
-          const int em = SB(SB_MODEL, s), ek_ = SB(SB_SIZE, s);
-#pragma unroll
-          for (int i = 0; i < NM; ++i) lp[i] += thr(em, ek_, i);
-        }
-      }
 #pragma unroll
       for (int i = 0; i < NM; ++i)
-        if (lp[i] + thr(m, k, i) > capf) return true;
+        if (GD(GD_LPA + i, g) + cd.c[i] > capf) return true;
     }
-    for (int p = 0; p < n; ++p) {
+    const int n = GI(GI_NRUN, g);
+    for (int p = 0; p < n; ++p) {  // projection of every equal-or-higher-priority co-runner (:137-160)
       const int s = slot_at(g, p);
       const int ep = SB(SB_PRIO, s);
       if (ep > cprio) continue;
-      const int em = SB(SB_MODEL, s), ek_ = SB(SB_SIZE, s);
       double nagg[NM];
 #pragma unroll
-      for (int i = 0; i < NM; ++i) nagg[i] = GD(GD_AGG + i, g) - thr(em, ek_, i) + thr(m, k, i);
-      const double cmp = tab_cmp(em, ek_), mem = tab_mem(em, ek_);
-      const double intf_new = pr.predict(nagg, cmp, mem, ep);
-      const double ks = SD(SD_KS, s);
-      double intf_cur;
-      if (SI(SI_ICP, s) == pass_id) {
-        intf_cur = SD(SD_ICUR, s);
-      } else {  // a function of (entry timeline, now, params) only: cached for the pass
-        double tw[NM];
-        tl_twa(s, now, tw);
-        intf_cur = pr.predict(tw, cmp, mem, ep);
-        SD(SD_ICUR, s) = intf_cur;
-        SI(SI_ICP, s) = pass_id;
-      }
-      const double tk = tab_kernel(em, ek_);
+      for (int i = 0; i < NM; ++i) nagg[i] = SD(SD_AEX + i, s) + cd.c[i];  // (agg - e.contrib) + add
+      const double intf_new = pr.predict(nagg, SD(SD_CMP, s), SD(SD_MEM, s), ep);
+      const double intf_cur = SD(SD_ICUR, s);
+      const double ks = SD(SD_KS, s), tk = SD(SD_TK, s);
       const double elapsed = py_max(0.0, now - ks);
       const double denom = intf_cur * tk;
       const double progress = denom > 0 ? py_min(1.0, elapsed / denom) : 1.0;
@@ -449,38 +466,27 @@ struct Sim {
     return false;
   }
 
+  // one (size, GPU) pair of best_for (scheduler.py:263-280): has_slot, violate, meet
+  __device__ __forceinline__ bool eval_pair(int g, const Cand& cd, int cprio, double dl, double front, double now,
+                                            double& lat, double& intf) const {
+    if (!(GI(GI_NRUN, g) < CONC)) return false;  // has_slot (runtime.py:101-102)
+    if (cf->use_violate && violate(g, cd, cprio, now)) return false;
+    double assumed[NM];  // check_meet (scheduler.py:164-185): half the aggregate
+#pragma unroll
+    for (int i = 0; i < NM; ++i) assumed[i] = 0.5 * GD(GD_AGG + i, g);
+    intf = pr.predict(assumed, cd.cmp, cd.mem, cprio);
+    lat = cd.total + py_max(0.0, GD(GD_TAV, g) - now) + (intf - 1.0) * cd.kern + (now - front);
+    return !(cf->use_meet && !(lat <= dl));
+  }
+
   struct Plan {
     bool ok;
     int gpu;
     double lat, intf;
   };
 
-  // best_for(k) (scheduler.py:263-280): lane per GPU, then the lexicographic
-  // (latency, gpu_id) argmin across lanes.
-  __device__ __forceinline__ Plan best_for(int m, int k, double front, double now, int pass_id) {
-    const int cprio = mprio(m);
-    const double cmp = tab_cmp(m, k), mem = tab_mem(m, k), total = tab_total(m, k), kern = tab_kernel(m, k);
-    const double dl = mdeadline(m);
-    const bool use_violate = cf->use_violate, use_meet = cf->use_meet;
-    bool found = false;
-    int bg = 0x7fffffff;
-    double bl = 0.0, bi = 0.0;
-    for (int g = lane; g < NG; g += 32) {
-      if (!(GI(GI_NRUN, g) < CONC)) continue;  // has_slot (runtime.py:101-102)
-      if (use_violate && violate(g, m, k, cprio, now, pass_id)) continue;
-      double assumed[NM];  // check_meet (scheduler.py:164-185)
-#pragma unroll
-      for (int i = 0; i < NM; ++i) assumed[i] = 0.5 * GD(GD_AGG + i, g);
-      const double intf = pr.predict(assumed, cmp, mem, cprio);
-      const double lat = total + py_max(0.0, GD(GD_TAV, g) - now) + (intf - 1.0) * kern + (now - front);
-      if (use_meet && !(lat <= dl)) continue;
-      if (!found || lat < bl) {
-        found = true;
-        bg = g;
-        bl = lat;
-        bi = intf;
-      }
-    }
+  // lexicographic (latency, gpu_id) argmin across the warp (best_for's tie-break)
+  __device__ __forceinline__ Plan warp_best(bool found, int bg, double bl, double bi) const {
 #pragma unroll
     for (int off = 16; off; off >>= 1) {
       const bool f2 = __shfl_xor_sync(kFull, found, off);
@@ -494,19 +500,87 @@ struct Sim {
         bi = i2;
       }
     }
-    sync();  // intf_cur cache writes
     return Plan{found, bg, bl, bi};
   }
 
+  // best_for(k) with lanes over GPUs
+  __device__ __forceinline__ Plan best_for(int m, int k, int cprio, double dl, double front, double now) const {
+    Cand cd;
+    load_cand(m, k, cd);
+    bool found = false;
+    int bg = 0x7fffffff;
+    double bl = 0.0, bi = 0.0;
+    for (int g = lane; g < NG; g += 32) {
+      double lat, intf;
+      if (eval_pair(g, cd, cprio, dl, front, now, lat, intf) && (!found || lat < bl)) {
+        found = true;
+        bg = g;
+        bl = lat;
+        bi = intf;
+      }
+    }
+    return warp_best(found, bg, bl, bi);
+  }
+
   // PredictivePolicy.propose (scheduler.py:257-285) + largest_feasible (:78-90).
-  // Probes never repeat, so the memo reduces to the plan of the last feasible probe.
-  __device__ __forceinline__ int propose(int m, double now, int pass_id, Plan& plan) {
+  // When every size fits in the warp (kmax segments of W = pow2ceil(n_gpus)
+  // lanes), all sizes are evaluated at once (lane = (k - 1) * W + g; best_for
+  // is pure, so evaluating sizes the search never probes changes nothing),
+  // each size's argmin is a segmented butterfly, and the binary search's exact
+  // probe sequence is replayed on the feasibility bits.  Otherwise sizes are probed one at a
+  // time with lanes over GPUs.  Probes never repeat, so the reference's memo
+  // reduces to the plan of the last feasible probe.
+  __device__ __forceinline__ int propose(int m, double now, Plan& plan) const {
     const double front = front_arrival(m);
     const int kmax = min(q_len(m), mmaxb(m));
+    const int cprio = mprio(m);
+    const double dl = mdeadline(m);
     int lo = 1, hi = kmax, bestk = 0;
+    // segment width: next power of two >= n_gpus
+    const int lw = NG <= 1 ? 0 : 32 - __clz(NG - 1);
+    if ((kmax << lw) <= 32) {
+      const int W = 1 << lw;
+      const int k = (lane >> lw) + 1, g = lane & (W - 1);
+      bool found = false;
+      int bg = g;
+      double bl = 0.0, bi = 0.0;
+      if (k <= kmax && g < NG) {
+        Cand cd;
+        load_cand(m, k, cd);
+        found = eval_pair(g, cd, cprio, dl, front, now, bl, bi);
+      }
+      // segmented lexicographic (latency, gpu_id) argmin within each size's W lanes
+      for (int off = W >> 1; off; off >>= 1) {
+        const bool f2 = __shfl_xor_sync(kFull, found, off);
+        const int g2 = __shfl_xor_sync(kFull, bg, off);
+        const double l2 = __shfl_xor_sync(kFull, bl, off);
+        const double i2 = __shfl_xor_sync(kFull, bi, off);
+        if (f2 && (!found || l2 < bl || (l2 == bl && g2 < bg))) {
+          found = true;
+          bg = g2;
+          bl = l2;
+          bi = i2;
+        }
+      }
+      const unsigned feas = __ballot_sync(kFull, found && g == 0);  // bit (k-1)*W: best_for(k) is not None
+      while (lo <= hi) {
+        const int mid = (lo + hi) / 2;
+        if (feas >> ((mid - 1) << lw) & 1u) {
+          bestk = mid;
+          lo = mid + 1;
+        } else {
+          hi = mid - 1;
+        }
+      }
+      if (bestk) {
+        const int src = (bestk - 1) << lw;
+        plan = Plan{true, __shfl_sync(kFull, bg, src), __shfl_sync(kFull, bl, src), __shfl_sync(kFull, bi, src)};
+      }
+      return bestk;
+    }
     while (lo <= hi) {
       const int mid = (lo + hi) / 2;
-      const Plan p = best_for(m, mid, front, now, pass_id);
+      const Plan p = best_for(m, mid, cprio, dl, front, now);
       if (p.ok) {
         bestk = mid;
         plan = p;
@@ -586,7 +660,11 @@ struct Sim {
       SB(SB_TLEN, s) = 0;
       SI(SI_BID, s) = bid;
       SI(SI_REQ0, s) = h;
-      SI(SI_ICP, s) = -1;
+#pragma unroll
+      for (int i = 0; i < NM; ++i) SD(SD_CON + i, s) = thr(m, k, i);
+      SD(SD_CMP, s) = tab_cmp(m, k);
+      SD(SD_MEM, s) = tab_mem(m, k);
+      SD(SD_TK, s) = tab_kernel(m, k);
       SD(SD_DL, s) = front + mdeadline(m);
       SD(SD_KS, s) = end;  // kernel_start_estimate
       SD(SD_REM, s) = tab_kernel(m, k);
@@ -636,42 +714,49 @@ struct Sim {
     ++c_passes;
     // queue_order (scheduler.py:249-255): stable sort of the ready queues by
     // (priority, front arrival, model_id), as a lane-parallel rank sort.
+    // key = priority in the top bit | bit pattern of the (>= 0) front arrival;
+    // queues that are not ready get ~0 and sort last.
+    unsigned long long* qk = reinterpret_cast<unsigned long long*>(qd);
+    const bool use_prio = cf->use_priority_order;
     for (int m = lane; m < M; m += 32) {
       const bool rdy = q_len(m) > 0;
-      qb[m] = rdy;
-      qd[m] = rdy ? front_arrival(m) : 0.0;
+      qk[m] = rdy ? ((unsigned long long)(use_prio ? mprio(m) : 0) << 63) |
+                        (unsigned long long)__double_as_longlong(front_arrival(m))
+                  : kNoKey;
     }
     sync();
-    const bool use_prio = cf->use_priority_order;
     int n = 0;
     for (int m0 = 0; m0 < M; m0 += 32) {
       const int m = m0 + lane;
-      const bool rdy = m < M && qb[m];
+      const unsigned long long km = m < M ? qk[m] : kNoKey;
+      const bool rdy = km != kNoKey;
       if (rdy) {
-        const int pm = use_prio ? mprio(m) : 0;
-        const double fm = qd[m];
         int rank = 0;
         for (int j = 0; j < M; ++j) {
-          if (!qb[j] || j == m) continue;
-          const int pj = use_prio ? mprio(j) : 0;
-          const double fj = qd[j];
-          rank += pj != pm ? pj < pm : (fj != fm ? fj < fm : j < m);
+          const unsigned long long kj = qk[j];
+          rank += kj < km || (kj == km && j < m);
         }
         QI(QI_ORD, rank) = m;
       }
       n += __popc(__ballot_sync(kFull, rdy));
     }
     sync();
+    bool icur_ready = false;
     for (int i = 0; i < n && !err; ++i) {
       const int m = QI(QI_ORD, i);
       early_drop(m, now);
       const int len = q_len(m);
       if (!len) continue;
       if (!(len >= mmaxb(m) || now >= front_arrival(m) + mtimeout(m))) continue;  // TaskQueue.eligible
+      if (!icur_ready) {
+        icur_all(now);
+        icur_ready = true;
+      }
       Plan plan;
-      const int k = propose(m, now, pass_id, plan);
+      const int k = propose(m, now, plan);
       if (!k) continue;
       submit(m, k, plan, now, pass_id);
+      icur_gpu(plan.gpu, now);
     }
     // _ensure_timeout for every queue in model order (simulation.py:360-361)
     for (int m0 = 0; m0 < M; m0 += 32) {
@@ -717,13 +802,11 @@ struct Sim {
       SB(SB_STARTED, s) = 1;
       SD(SD_KS, s) = now;  // kernel_start (and kernel_start_estimate)
       SB(SB_TLEN, s) = 0;  // timeline reset to the kernel window
-      double v[NM];
-      const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s);
+      double v[NM];  // timeline reset to [(now, aggregate_excluding(entry))]
 #pragma unroll
-      for (int i = 0; i < NM; ++i) v[i] = GD(GD_AGG + i, g) - thr(m, k, i);
+      for (int i = 0; i < NM; ++i) v[i] = SD(SD_AEX + i, s);
       tl_record(s, now, v);
-      SI(SI_ICP, s) = -1;
-      SD(SD_SLOW, s) = gt_slowdown(g, s);
+      SD(SD_SLOW, s) = gt_slowdown(s);
       SD(SD_LAST, s) = now;
       A->b_kernel_start[base + SI(SI_BID, s)] = now;
     }
@@ -846,12 +929,9 @@ struct Sim {
       GI(GI_PHEAD, g) = 0;
       GI(GI_PN, g) = 0;
 #pragma unroll
-      for (int i = 0; i < NM; ++i) GD(GD_AGG + i, g) = 0.0;
+      for (int i = 0; i < NM; ++i) GD(GD_AGG + i, g) = GD(GD_LPA + i, g) = 0.0;
     }
-    for (int s = lane; s < S; s += 32) {
-      SB(SB_LIVE, s) = 0;
-      SI(SI_ICP, s) = -1;
-    }
+    for (int s = lane; s < S; s += 32) SB(SB_LIVE, s) = 0;
     for (int i = lane; i < NE; i += 32) {
       ed[i] = INF;
       ek[i] = kNoKey;
@@ -895,14 +975,24 @@ struct Sim {
         const unsigned long long kk = ek[i];
         if (t < bt || (t == bt && kk < bk)) bt = t, bk = kk, bi = i;
       }
-#pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        const double t2 = __shfl_xor_sync(kFull, bt, off);
-        const unsigned long long k2 = __shfl_xor_sync(kFull, bk, off);
-        const int i2 = __shfl_xor_sync(kFull, bi, off);
-        if (t2 < bt || (t2 == bt && k2 < bk)) bt = t2, bk = k2, bi = i2;
+      // across lanes: event times are >= 0, so their bit patterns order like the
+      // values; a 128-bit (time, key) minimum as four 32-bit warp reductions
+      {
+        const unsigned long long tb = (unsigned long long)__double_as_longlong(bt);
+        const unsigned w0 = (unsigned)(tb >> 32), w1 = (unsigned)tb, w2 = (unsigned)(bk >> 32), w3 = (unsigned)bk;
+        const unsigned m0 = __reduce_min_sync(kFull, w0);
+        bool c = w0 == m0;
+        const unsigned m1 = __reduce_min_sync(kFull, c ? w1 : ~0u);
+        c = c && w1 == m1;
+        const unsigned m2 = __reduce_min_sync(kFull, c ? w2 : ~0u);
+        c = c && w2 == m2;
+        const unsigned m3 = __reduce_min_sync(kFull, c ? w3 : ~0u);
+        c = c && w3 == m3;
+        bk = ((unsigned long long)m2 << 32) | m3;
+        if (bk == kNoKey) break;
+        bt = __longlong_as_double((long long)(((unsigned long long)m0 << 32) | m1));
+        bi = __shfl_sync(kFull, bi, __ffs(__ballot_sync(kFull, c)) - 1);
       }
-      if (bk == kNoKey) break;
       const int kind = (int)(bk >> 56);
       const double now = bt;
       ++c_events;
@@ -978,8 +1068,11 @@ struct Sim {
   }
 };
 
-template <int NM>
-__global__ void __launch_bounds__(128) replay_kernel(const __grid_constant__ StraitReplayArgs a, int wpc) {
+// MINB = minimum resident CTAs of 4 warps per SM: 1 lets ptxas keep the whole
+// replay state in registers (latency: few replays), 4 caps it at 128 registers
+// for 16 resident replays per SM (throughput: replay sweeps).
+template <int NM, int MINB>
+__global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant__ StraitReplayArgs a, int wpc) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int w = threadIdx.x >> 5;
   const int64_t r = (int64_t)blockIdx.x * wpc + w;
@@ -1024,16 +1117,27 @@ __global__ void __launch_bounds__(128) replay_kernel(const __grid_constant__ Str
 template <int NM>
 int launch_replay(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp);
 
-#define STRAIT_INSTANTIATE_REPLAY(NMV)                                                                      \
-  template <>                                                                                               \
-  int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) {       \
-    const size_t smem = smem_per_warp * wpc;                                                                \
-    if (cudaFuncSetAttribute(replay_kernel<NMV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != \
-        cudaSuccess)                                                                                        \
-      return set_error(STRAIT_ECUDA, "strait_replay: cannot reserve %zu B of shared memory", smem);         \
-    const unsigned grid = (unsigned)((a.n_replays + wpc - 1) / wpc);                                        \
-    replay_kernel<NMV><<<grid, 32 * wpc, smem, st>>>(a, wpc);                                               \
-    return check_launch("strait_replay");                                                                   \
+template <int NM, int MINB>
+int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) {
+  const size_t smem = smem_per_warp * wpc;
+  if (cudaFuncSetAttribute(replay_kernel<NM, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return set_error(STRAIT_ECUDA, "strait_replay: cannot reserve %zu B of shared memory", smem);
+  const unsigned grid = (unsigned)((a.n_replays + wpc - 1) / wpc);
+  replay_kernel<NM, MINB><<<grid, 32 * wpc, smem, st>>>(a, wpc);
+  return check_launch("strait_replay");
+}
+
+// occupancy variant: env STRAIT_REPLAY_OCC=1|4 forces one; default picks the
+// high-occupancy kernel once there are more replays than the latency kernel
+// can keep resident (2 CTAs x 4 warps per SM).
+int replay_occupancy(int64_t n_replays, int wpc);
+
+#define STRAIT_INSTANTIATE_REPLAY(NMV)                                                                \
+  template <>                                                                                         \
+  int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) { \
+    return replay_occupancy(a.n_replays, wpc) >= 4 ? launch_replay_occ<NMV, 4>(a, st, wpc, smem_per_warp) \
+                                                   : launch_replay_occ<NMV, 1>(a, st, wpc, smem_per_warp); \
   }
 
 }  // namespace rp
