@@ -13,7 +13,7 @@ OBJS := $(patsubst paper_2604_28175_b200/csrc/%.cu,build/%.o,$(CSRC))
 all: $(LIB)
 
 CDIR := paper_2604_28175_b200/csrc
-COMMON_HDR := $(CDIR)/strait_device.cuh $(CDIR)/strait_capi.cuh include/strait.h
+COMMON_HDR := $(CDIR)/strait_device.cuh $(CDIR)/strait_capi.cuh $(CDIR)/strait_libm.cuh $(CDIR)/strait_libm_tables.cuh include/strait.h
 SWEEP_HDR := $(COMMON_HDR) $(CDIR)/strait_ptx.cuh $(CDIR)/strait_refit.cuh
 REPLAY_HDR := $(COMMON_HDR) $(CDIR)/strait_replay_impl.cuh include/strait_replay.h
 

@@ -64,6 +64,15 @@ int strait_last_sweep_path(void);
 void strait_host_exp(const double *x, double *y, int64_t n);
 
 /*
+ * Elementwise device math with the reference host's bits: fn 0 exp(x),
+ * 1 log(x), 2 pow(x, y) — restatements of glibc 2.39's exp/log/pow (the
+ * libm behind CPython's math.exp, math.log and float.__pow__, which
+ * predictor.py:136-137,181-184,289-293 and oracle.py:73 call).  y may be NULL
+ * unless fn == 2.
+ */
+int strait_math(int32_t fn, const double *x, const double *y, int64_t n, double *out, void *stream);
+
+/*
  * R1-R3: batched predict_interference (predictor.py:208-216).
  *   coloc [n_metrics][n], self_cmp[n], self_mem[n], prio[n] -> out_intf[n],
  *   out_saturated[n] (the _raw_effect saturation flag, predictor.py:179-185;

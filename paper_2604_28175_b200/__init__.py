@@ -16,5 +16,9 @@ from .predictor import (FeedbackSample, InterferencePredictor, OptimizerState, P
                         pressure_exponent)
 from .profiles import default_profiles, load_profile, random_profile, save_profile
 from .runtime import AimdState, GpuRuntimeState, RunningTaskEntry
+from .scheduler import (BatchPlan, PredictivePolicy, ScheduleDecision, SchedulingPolicy, TaskQueue, check_meet,
+                        check_violate, complete_batch, early_drop, largest_feasible, make_policy, run_scheduling_pass,
+                        submit_plan)
+from .simulation import SimResult, Simulation, run, run_many
 
 __version__ = "0.1.0"

@@ -148,6 +148,8 @@ def _declare(lib):
     lib.strait_refit.argtypes = [C.POINTER(RefitArgs), _vp]
     lib.strait_round.restype = C.c_int
     lib.strait_round.argtypes = [C.POINTER(SweepArgs), C.POINTER(RefitArgs), _vp]
+    lib.strait_math.restype = C.c_int
+    lib.strait_math.argtypes = [C.c_int32, _vp, _vp, C.c_int64, _vp, _vp]
     lib.strait_host_exp.restype = None
     lib.strait_host_exp.argtypes = [_vp, _vp, C.c_int64]
     if hasattr(lib, "strait_replay"):

@@ -4,16 +4,32 @@
 // /root/reference/pkg/src/infersim) in its exact left-to-right evaluation
 // order.  The library is compiled with --fmad=false -prec-div=true
 // -prec-sqrt=true so that each `a * b + c` below rounds twice, like CPython.
-// The only deviations from the reference are libdevice exp/log/pow (<= 1-2 ulp
-// from glibc on a small fraction of inputs), which the parity tests bound.
+// exp/log/pow are restatements of the reference host's glibc routines
+// (strait_libm.cuh), so results are bit-identical to the reference.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "../../include/strait.h"
+#include "strait_libm.cuh"
 
 namespace strait {
+
+// exp / log / pow with the reference host's bits (strait_libm.cuh).  Build with
+// -DSTRAIT_LIBM=0 to use libdevice instead (<= 1-2 ulp, for A/B timing only).
+#ifndef STRAIT_LIBM
+#define STRAIT_LIBM 1
+#endif
+#if STRAIT_LIBM
+__device__ __forceinline__ double dexp(double x) { return glibc::exp(x); }
+__device__ __forceinline__ double dlog(double x) { return glibc::log(x); }
+__device__ __forceinline__ double dpow(double x, double y) { return glibc::pow(x, y); }
+#else
+__device__ __forceinline__ double dexp(double x) { return ::exp(x); }
+__device__ __forceinline__ double dlog(double x) { return ::log(x); }
+__device__ __forceinline__ double dpow(double x, double y) { return ::pow(x, y); }
+#endif
 
 constexpr double kLogSaturate = 500.0;  // predictor.py:27 _LOG_SATURATE
 constexpr int kMaxM = STRAIT_MAX_METRICS;
@@ -34,7 +50,7 @@ struct Pred {
 
   __device__ __forceinline__ void load(const double* __restrict__ P, double effect_cap) {
     scale = P[0];
-    log_base = log(P[1]);
+    log_base = dlog(P[1]);
     offset = P[2];
 #pragma unroll
     for (int i = 0; i < NM; ++i) w[i] = P[3 + i];
@@ -60,7 +76,7 @@ struct Pred {
       saturated = true;
       return cap;
     }
-    const double inner = scale * exp(z) + offset;
+    const double inner = scale * dexp(z) + offset;
     saturated = inner >= cap;
     if (saturated) return cap;
     return py_min(py_max(inner, 0.0), cap);

@@ -1,0 +1,28 @@
+// strait_math.cu — elementwise device exp / log / pow (strait_libm.cuh), the
+// transcendental functions of the estimator (predictor.py:181-184,289-293)
+// and the ground truth (oracle.py:73), exported so their bit-identity with the
+// host libm can be checked directly (tests/test_libm_gpu.py).
+#include <cuda_runtime.h>
+
+#include "strait_capi.cuh"
+#include "strait_device.cuh"
+
+namespace {
+__global__ void math_kernel(int fn, const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                            double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = x[i];
+    out[i] = fn == 0 ? strait::dexp(a) : fn == 1 ? strait::dlog(a) : strait::dpow(a, y[i]);
+  }
+}
+}  // namespace
+
+extern "C" int strait_math(int32_t fn, const double* x, const double* y, int64_t n, double* out, void* stream) {
+  if (fn < 0 || fn > 2 || n < 0 || (n && (!x || !out || (fn == 2 && !y))))
+    return strait::set_error(STRAIT_EINVAL, "strait_math: bad arguments");
+  if (!n) return STRAIT_OK;
+  const int64_t blocks64 = (n + 255) / 256;
+  const unsigned blocks = (unsigned)(blocks64 < 4096 ? blocks64 : 4096);
+  math_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(fn, x, y, n, out);
+  return strait::check_launch("strait_math");
+}

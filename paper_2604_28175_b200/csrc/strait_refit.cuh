@@ -43,7 +43,7 @@ __device__ void refit_warp(const StraitRefitArgs& a, double* sP /* shared, >= NM
     double x = sP[3 + NM] * cmp + sP[4 + NM] * mem;
 #pragma unroll
     for (int k = 0; k < NM; ++k) x += sP[3 + k] * tw[k];
-    const double log_b = log(base);
+    const double log_b = dlog(base);
     const double z = x * log_b;
     bool saturated;
     double inner, pow_bx = 0.0;
@@ -51,7 +51,7 @@ __device__ void refit_warp(const StraitRefitArgs& a, double* sP /* shared, >= NM
       saturated = true;
       inner = __longlong_as_double(0x7ff0000000000000LL);  // math.inf
     } else {
-      pow_bx = exp(z);
+      pow_bx = dexp(z);
       inner = scale * pow_bx + offset;
       saturated = inner >= cap;
     }
@@ -66,7 +66,7 @@ __device__ void refit_warp(const StraitRefitArgs& a, double* sP /* shared, >= NM
     if (!clamp_active && owner) {
       const double zz = scale * pow_bx;
       if (lane == 0) d = pow_bx * cf;
-      else if (lane == 1) d = scale * x * exp((x - 1.0) * log_b) * cf;
+      else if (lane == 1) d = scale * x * dexp((x - 1.0) * log_b) * cf;
       else if (lane == 2) d = cf;
       else if (lane < 3 + NM) {
         double ai = 0.0;

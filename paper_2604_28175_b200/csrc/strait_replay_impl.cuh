@@ -29,7 +29,8 @@
 //    (ballot-ordered).  Everything else is uniform scalar code executed by all
 //    lanes; shared-memory scalars are written by lane 0 followed by __syncwarp.
 //  * Binary64 throughout, --fmad=false, left-to-right evaluation as the
-//    reference; the only deviation is libdevice exp/log/pow vs glibc.
+//    reference, exp/log/pow restated from the reference host's glibc
+//    (strait_libm.cuh): results are bit-identical to the reference.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -265,7 +266,7 @@ struct Sim {
     double x = cf->gt_w_cmp * SD(SD_CMP, s) + cf->gt_w_mem * SD(SD_MEM, s);
 #pragma unroll
     for (int i = 0; i < NM; ++i) x += cf->gt_w[i] * SD(SD_AEX + i, s);
-    double effect = cf->gt_family == 0 ? cf->gt_scale * pow(cf->gt_base, x) + cf->gt_offset
+    double effect = cf->gt_family == 0 ? cf->gt_scale * dpow(cf->gt_base, x) + cf->gt_offset
                                        : cf->gt_scale * x * x + cf->gt_offset;
     effect = py_max(0.0, effect);
     return 1.0 + effect * (SB(SB_PRIO, s) == 0 ? cf->gt_pf_high : cf->gt_pf_low) * SD(SD_NOISE, s);
@@ -349,7 +350,7 @@ struct Sim {
       saturated = true;
       inner = __longlong_as_double(0x7ff0000000000000LL);
     } else {
-      pow_bx = exp(z);
+      pow_bx = dexp(z);
       inner = pr.scale * pow_bx + pr.offset;
       saturated = inner >= cap;
     }
@@ -363,7 +364,7 @@ struct Sim {
       const double log_b = pr.log_base;
       const double zz = pr.scale * pow_bx;
       if (lane == 0) d = pow_bx * cfc;
-      else if (lane == 1) d = pr.scale * x * exp((x - 1.0) * log_b) * cfc;
+      else if (lane == 1) d = pr.scale * x * dexp((x - 1.0) * log_b) * cfc;
       else if (lane == 2) d = cfc;
       else if (lane < 3 + NM) {
         double ai = 0.0;
