@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replay-steps", type=int, default=3, help="timed launches of the C4 replay sweep")
+    ap.add_argument("--replay-seeds", type=int, default=16, help="seeds per C4 grid point (16 = BASELINE C4)")
+    ap.add_argument("--no-replay", action="store_true")
     return ap.parse_args()
 
 
@@ -145,6 +148,134 @@ def cpu_round_rate(soa, fb, seconds: float, threads: int):
     return preds / dt, dt, segs
 
 
+# ----------------------------------------------------------------------------- C4 replay sweep
+REPLAY_UNIT = "simulated requests/s"
+
+
+def c4_shard(args, ws, rank):
+    """BASELINE configs[3]: 8 loads x 8 HP fractions x seeds replays of overload's
+    3 s horizon; replay r runs on rank r mod N (strong scaling)."""
+    from paper_2604_28175_b200.configs import c4_grid
+    from paper_2604_28175_b200.replay import ReplaySpec
+    from paper_2604_28175_b200.shard import shard
+
+    grid = c4_grid(seeds=args.replay_seeds)
+    return [ReplaySpec(c, s) for c, s in shard(grid, ws, rank)], len(grid)
+
+
+def replay_cpu(specs, seconds: float, threads: int):
+    """Oracle port (oracle/strait_replay_oracle.c, OpenMP over replays) on an
+    evenly strided subset of the sweep holding ~`seconds` of host work."""
+    from oracle import oracle
+    from paper_2604_28175_b200.replay import ReplayBatch
+
+    budget = seconds * 350_000 * threads  # requests, at the oracle's ~350k req/s/core
+    per = max(1, int(ReplayBatch(specs[:1]).N))
+    k = max(1, int(budget // per))
+    sub = specs[:: max(1, len(specs) // k)][:k]
+    batch = ReplayBatch(sub)
+    t0 = time.perf_counter()
+    res = oracle.replay(batch, threads=threads)
+    dt = time.perf_counter() - t0
+    assert (res.counters[:, 0] == 0).all()
+    return batch.N / dt, dt, len(sub), batch.N
+
+
+def replay_leg(args, ws, rank, local, dist):
+    """Device time of the whole C4 sweep (inputs resident) + the same through
+    the public API with host buffers (pinned H2D of every input, D2H of the
+    per-request outcomes and counters)."""
+    import ctypes as Cc
+
+    import torch
+
+    from paper_2604_28175_b200 import _device as D
+    from paper_2604_28175_b200.replay import RC, ReplayBatch
+
+    specs, n_total = c4_shard(args, ws, rank)
+    t0 = time.perf_counter()
+    batch = ReplayBatch(specs)
+    build_s = time.perf_counter() - t0
+    lib = D.lib()
+    host_in = batch.host_inputs()
+    din = batch.device_inputs()
+    dout = batch.alloc_outputs(device=True)
+    cargs = batch.args(din, dout, D.ptr)
+    st0, sp0 = din["pred_state"].clone(), din["pred_step"].clone()
+    stream = torch.cuda.current_stream()
+
+    def launch():
+        din["pred_state"].copy_(st0)
+        din["pred_step"].copy_(sp0)
+        D.check(lib.strait_replay(Cc.byref(cargs), stream.cuda_stream))
+
+    launch()  # warm-up (module load, smem carve-out)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    l0 = lib.strait_kernel_launches()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(args.replay_steps):
+        launch()
+    ev[1].record()
+    torch.cuda.synchronize()
+    dev_ms = ev[0].elapsed_time(ev[1]) / args.replay_steps
+    launches = (lib.strait_kernel_launches() - l0) / args.replay_steps
+    counters = D.host(dout["counters"]).reshape(batch.R, -1)
+    assert (counters[:, RC["ERROR"]] == 0).all(), "replay error"
+    # end to end through the C-ABI with host buffers
+    keys = [k for k in host_in if k != "cfg"]
+    pinned = {k: torch.from_numpy(np.ascontiguousarray(host_in[k])).pin_memory() for k in keys}
+    pinned["cfg"] = torch.frombuffer(bytearray(bytes(host_in["cfg"])), dtype=torch.uint8).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in pinned.values())
+    outs = ("counters", "req_status", "req_violated")
+    hout = {k: torch.empty(dout[k].shape, dtype=dout[k].dtype, pin_memory=True) for k in outs}
+    d2h = sum(t.numel() * t.element_size() for t in hout.values())
+    e2e = []
+    for i in range(2):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k, t in pinned.items():
+            din[k].copy_(t, non_blocking=True)
+        D.check(lib.strait_replay(Cc.byref(cargs), stream.cuda_stream))
+        for k in outs:
+            hout[k].copy_(dout[k], non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        if i:
+            e2e.append(e0.elapsed_time(e1))
+    c = hout["counters"].numpy().reshape(batch.R, -1)
+    vec = torch.tensor([dev_ms, e2e[0], build_s, 0, 0, 0, 0, 0, 0], dtype=torch.float64, device="cuda")
+    vec[3:] = torch.tensor([batch.N, c[:, RC["HP_ARR"]].sum(), c[:, RC["LP_ARR"]].sum(), c[:, RC["HP_VIOL"]].sum(),
+                            c[:, RC["LP_VIOL"]].sum(), c[:, RC["BATCHES"]].sum()], dtype=torch.float64)
+    if ws > 1:  # the only collective: max of the times, sum of the counters (NCCL)
+        mx, sm = vec[:3].clone(), vec[3:].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        vec = torch.cat([mx, sm])
+    dev_ms, e2e_ms, build_s, n_req, hp_arr, lp_arr, hp_v, lp_v, nb = vec.tolist()
+    out = {"workload": f"C4 load x HP-fraction sweep (BASELINE configs[3]): {n_total} replays of overload.yaml "
+                       f"(3 s, 6 models x 4 GPUs), replay r on rank r mod {ws}",
+           "value": n_req / (dev_ms / 1e3), "unit": REPLAY_UNIT, "ms_per_step": dev_ms, "steps": args.replay_steps,
+           "replays": n_total, "requests": int(n_req), "batches": int(nb), "scaling": "strong",
+           "hp_violation_pct": 100.0 * hp_v / max(hp_arr, 1), "lp_violation_pct": 100.0 * lp_v / max(lp_arr, 1),
+           "e2e": {"value": n_req / (e2e_ms / 1e3), "unit": REPLAY_UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                   "path": "pinned host inputs -> H2D -> strait_replay (C-ABI) -> D2H outcomes"},
+           "host_input_build_s": build_s, "gpu_launches": launches,
+           "bound": "latency (one warp per replay); no roofline claim, DESIGN.md 3.3"}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, dt, nrep, nreq = replay_cpu(specs, args.cpu_seconds, threads)
+        out["cpu_baseline"] = {"value": rate, "unit": REPLAY_UNIT, "cores": threads, "kind": "port",
+                               "sample": f"{nrep} evenly strided replays of the sweep ({nreq} requests) in {dt:.1f}s "
+                                         f"on {threads} threads (oracle/strait_replay_oracle.c)"}
+    return out
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -169,6 +300,12 @@ def run_reference(args):
                                    f"per step on {threads} threads (OpenMP)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_replay:
+        specs, n_total = c4_shard(args, 1, 0)
+        rate, dt, nrep, nreq = replay_cpu(specs, t_budget / 3, threads)
+        line["replay"] = {"workload": f"C4 sweep ({n_total} replays), evenly strided sample", "value": rate,
+                          "unit": REPLAY_UNIT, "cores": threads, "kind": "port",
+                          "sample": f"{nrep} replays, {nreq} requests, {dt:.1f}s"}
     print(json.dumps(line), flush=True)
 
 
@@ -275,6 +412,7 @@ def run_ours(args):
         dist.all_reduce(sm[3:], op=dist.ReduceOp.SUM)
         vec = torch.cat([mx[:3], sm[3:]])
     elapsed_ms, e2e_step_ms, kern_ms_max, checksum = (float(x) for x in vec.tolist())
+    replay = None if args.no_replay else replay_leg(args, ws, rank, local, dist)
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()
@@ -304,6 +442,7 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": kern_ms},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
+        "replay": replay,
         "checksum": checksum,
     }
     if not args.no_cpu_baseline:

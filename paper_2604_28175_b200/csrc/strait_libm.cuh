@@ -22,7 +22,6 @@ namespace glibc {
 
 __device__ __forceinline__ double as_d(uint64_t u) { return __longlong_as_double((long long)u); }
 __device__ __forceinline__ uint64_t as_u(double d) { return (uint64_t)__double_as_longlong(d); }
-__device__ __forceinline__ double hdr(const uint64_t* t, int i) { return as_d(__ldg(&t[i])); }
 __device__ __forceinline__ uint32_t top12(double x) { return (uint32_t)(as_u(x) >> 52); }
 
 constexpr uint32_t kExpBits = 7;
@@ -53,19 +52,19 @@ __device__ __forceinline__ double exp_special(double tmp, uint64_t sbits, uint64
 // exp core shared by exp() and pow(): 2^(k/N) * exp(r), |r| <= ln2/2N
 template <bool POW>
 __device__ __forceinline__ double exp_core(double x, double xtail, uint64_t sign_bias, uint32_t abstop) {
-  const double InvLn2N = hdr(kExpHdr, 0), Shift = hdr(kExpHdr, 1);
-  const double NegLn2hiN = hdr(kExpHdr, 2), NegLn2loN = hdr(kExpHdr, 3);
-  const double C2 = hdr(kExpHdr, 4), C3 = hdr(kExpHdr, 5), C4 = hdr(kExpHdr, 6), C5 = hdr(kExpHdr, 7);
+  constexpr double InvLn2N = kExpInvLn2N, Shift = kExpShift;
+  constexpr double NegLn2hiN = kExpNegLn2hiN, NegLn2loN = kExpNegLn2loN;
+  constexpr double C2 = kExpC2, C3 = kExpC3, C4 = kExpC4, C5 = kExpC5;
   double kd = __fma_rn(x, InvLn2N, Shift);  // fma: z = InvLn2N * x; kd = z + Shift
   const uint64_t ki = as_u(kd);
   kd -= Shift;
   double r = __fma_rn(kd, NegLn2hiN, x);  // fma
   r = __fma_rn(kd, NegLn2loN, r);         // fma
   if (POW) r = xtail + r;                 // pow's exp_inline: r += xtail
-  const uint64_t idx = 2 * (ki % kN);
   const uint64_t top = (ki + sign_bias) << (52 - kExpBits);
-  const double tail = as_d(__ldg(&kExpTab[idx]));
-  const uint64_t sbits = __ldg(&kExpTab[idx + 1]) + top;
+  const ulonglong2 te = __ldg(reinterpret_cast<const ulonglong2*>(kExpTab) + (ki % kN));  // one 16-B load
+  const double tail = as_d(te.x);
+  const uint64_t sbits = te.y + top;
   const double r2 = r * r;
   const double p23 = __fma_rn(r, C3, C2);       // fma
   const double p45 = __fma_rn(r, C5, C4);       // fma
@@ -101,13 +100,13 @@ __device__ __forceinline__ double log(double x) {
     const double r = x - 1.0;
     const double r2 = r * r;
     const double r3 = r * r2;
-    const double B0 = hdr(kLogHdr, 7);
-    double p = __fma_rn(r, hdr(kLogHdr, 15), hdr(kLogHdr, 14));           // B7 + r*B8
-    p = __fma_rn(r2, hdr(kLogHdr, 16), p);                                 // + r2*B9
-    p = __fma_rn(r3, hdr(kLogHdr, 17), p);                                 // + r3*B10
-    const double q4 = __fma_rn(r2, hdr(kLogHdr, 13), __fma_rn(r, hdr(kLogHdr, 12), hdr(kLogHdr, 11)));
+    const double B0 = kLogB0;
+    double p = __fma_rn(r, kLogB8, kLogB7);           // B7 + r*B8
+    p = __fma_rn(r2, kLogB9, p);                                 // + r2*B9
+    p = __fma_rn(r3, kLogB10, p);                                 // + r3*B10
+    const double q4 = __fma_rn(r2, kLogB6, __fma_rn(r, kLogB5, kLogB4));
     p = __fma_rn(p, r3, q4);                                               // B4 + r*B5 + r2*B6 + r3*(...)
-    const double q1 = __fma_rn(r2, hdr(kLogHdr, 10), __fma_rn(r, hdr(kLogHdr, 9), hdr(kLogHdr, 8)));
+    const double q1 = __fma_rn(r2, kLogB3, __fma_rn(r, kLogB2, kLogB1));
     p = __fma_rn(p, r3, q1);                                               // B1 + r*B2 + r2*B3 + r3*(...)
     const double rhi = __fma_rn(-0x1p27, r, __fma_rn(r, 0x1p27, r));     // w = r*2^27; rhi = r + w - w
     const double rlo = r - rhi;
@@ -129,18 +128,19 @@ __device__ __forceinline__ double log(double x) {
   const int i = (int)((tmp >> 45) % 128);
   const int k = (int)((int64_t)tmp >> 52);
   const uint64_t iz = ix - (tmp & (0xfffull << 52));
-  const double invc = as_d(__ldg(&kLogTab[2 * i])), logc = as_d(__ldg(&kLogTab[2 * i + 1]));
+  const double2 tl = __ldg(reinterpret_cast<const double2*>(kLogTab) + i);  // (invc, logc)
+  const double invc = tl.x, logc = tl.y;
   const double z = as_d(iz);
   const double kd = (double)k;
   const double r = __fma_rn(z, invc, -1.0);                     // fma (__FP_FAST_FMA path)
-  const double w = __fma_rn(kd, hdr(kLogHdr, 0), logc);          // fma: kd*Ln2hi + logc
+  const double w = __fma_rn(kd, kLogLn2hi, logc);          // fma: kd*Ln2hi + logc
   const double hi = r + w;
   double lo = w - hi + r;
-  lo = __fma_rn(kd, hdr(kLogHdr, 1), lo);                        // fma: + kd*Ln2lo
+  lo = __fma_rn(kd, kLogLn2lo, lo);                        // fma: + kd*Ln2lo
   const double r2 = r * r;
-  const double a12 = __fma_rn(r, hdr(kLogHdr, 4), hdr(kLogHdr, 3));  // A1 + r*A2
-  const double a34 = __fma_rn(r, hdr(kLogHdr, 6), hdr(kLogHdr, 5));  // A3 + r*A4
-  const double lo2 = __fma_rn(r2, hdr(kLogHdr, 2), lo);              // lo + r2*A0
+  const double a12 = __fma_rn(r, kLogA2, kLogA1);  // A1 + r*A2
+  const double a34 = __fma_rn(r, kLogA4, kLogA3);  // A3 + r*A4
+  const double lo2 = __fma_rn(r2, kLogA0, lo);              // lo + r2*A0
   const double poly = __fma_rn(a34, r2, a12);                        // A1 + r*A2 + r2*(A3 + r*A4)
   return __fma_rn(r * r2, poly, lo2) + hi;
 }
@@ -154,22 +154,23 @@ __device__ __forceinline__ double pow_log(uint64_t ix, double& tail) {
   const uint64_t iz = ix - (tmp & (0xfffull << 52));
   const double z = as_d(iz);
   const double kd = (double)k;
-  const double invc = as_d(__ldg(&kPowTab[4 * i])), logc = as_d(__ldg(&kPowTab[4 * i + 2]));
-  const double logctail = as_d(__ldg(&kPowTab[4 * i + 3]));
+  const double2 ta = __ldg(reinterpret_cast<const double2*>(kPowTab) + 2 * i);      // (invc, pad)
+  const double2 tb = __ldg(reinterpret_cast<const double2*>(kPowTab) + 2 * i + 1);  // (logc, logctail)
+  const double invc = ta.x, logc = tb.x, logctail = tb.y;
   const double r = __fma_rn(z, invc, -1.0);                     // fma
-  const double t1 = __fma_rn(kd, hdr(kPowHdr, 0), logc);         // fma: kd*Ln2hi + logc
+  const double t1 = __fma_rn(kd, kPowLn2hi, logc);         // fma: kd*Ln2hi + logc
   const double t2 = r + t1;
-  const double lo1 = __fma_rn(kd, hdr(kPowHdr, 1), logctail);    // fma: kd*Ln2lo + logctail
+  const double lo1 = __fma_rn(kd, kPowLn2lo, logctail);    // fma: kd*Ln2lo + logctail
   const double lo2 = t1 - t2 + r;
-  const double ar = r * hdr(kPowHdr, 2);  // A[0] * r
+  const double ar = r * kPowA0;  // A[0] * r
   const double ar2 = r * ar;
   const double ar3 = r * ar2;
   const double hi = t2 + ar2;
   const double lo3 = __fma_rn(ar, r, -ar2);  // fma
   const double lo4 = t2 - hi + ar2;
-  const double a12 = __fma_rn(r, hdr(kPowHdr, 4), hdr(kPowHdr, 3));  // A1 + r*A2
-  const double a34 = __fma_rn(r, hdr(kPowHdr, 6), hdr(kPowHdr, 5));  // A3 + r*A4
-  const double a56 = __fma_rn(r, hdr(kPowHdr, 8), hdr(kPowHdr, 7));  // A5 + r*A6
+  const double a12 = __fma_rn(r, kPowA2, kPowA1);  // A1 + r*A2
+  const double a34 = __fma_rn(r, kPowA4, kPowA3);  // A3 + r*A4
+  const double a56 = __fma_rn(r, kPowA6, kPowA5);  // A5 + r*A6
   const double q = __fma_rn(ar2, __fma_rn(a56, ar2, a34), a12);      // A1 + r*A2 + ar2*(A3 + r*A4 + ar2*(A5 + r*A6))
   const double lo = __fma_rn(ar3, q, lo1 + lo2 + lo3 + lo4);          // fma: lo1 + lo2 + lo3 + lo4 + ar3*q
   const double y = hi + lo;

@@ -5,72 +5,11 @@ reference's own loaders (the shipped pkg/configs YAMLs, restated here as
 dicts; the example trace's per-minute counts likewise)."""
 from __future__ import annotations
 
-import math
-
-import numpy as np
-
 from paper_2604_28175_b200 import config as MC
-from paper_2604_28175_b200.domain import PriorityLevel
-from paper_2604_28175_b200.profiles import random_profile
-from paper_2604_28175_b200.workload import ModelWorkload
-
-# pkg/configs/example_trace.csv (per-minute counts)
-EXAMPLE_TRACE = {"vision_gate": {0: 7654.0, 1: 11412.0, 2: 7322.0, 3: 7268.0, 4: 8189.0},
-                 "doc_reader": {0: 2514.0, 1: 3306.0, 2: 2307.0, 3: 3713.0, 4: 3644.0}}
-
-DEMO = {"profiles": "default6", "duration_ms": 1000, "seed": 1, "n_gpus": 1, "policy": "predictive",
-        "ground_truth": {"noise_sigma": 0.05},
-        "workload": {"resnet50": {"mode": "poisson", "rate": 300}, "yolo_v8n": {"mode": "uniform", "rate": 150},
-                     "roberta_b": {"mode": "poisson", "rate": 80}}}
-C1 = {"profiles": "default6", "duration_ms": 26316, "seed": 1, "n_gpus": 1, "policy": "predictive",
-      "ground_truth": {"noise_sigma": 0.05},
-      "workload": {"resnet50": {"mode": "poisson", "rate": 300}, "roberta_b": {"mode": "poisson", "rate": 80}}}
-OVERLOAD_GT = {"family": "exponential", "scale": 0.5, "base": 2.718281828459045, "offset": -0.7686,
-               "weights": [0.3] * 5, "self_compute_weight": 0.25, "self_memory_weight": 0.2,
-               "priority_factor": {"high": 0.6, "low": 1.0}, "noise_sigma": 0.05}
-OVERLOAD_WL = {"resnet50": {"mode": "poisson", "rate": 2200}, "vit_b16": {"mode": "poisson", "rate": 800},
-               "yolo_v8n": {"mode": "poisson", "rate": 1300}, "convnext_b": {"mode": "poisson", "rate": 650},
-               "vgg19": {"mode": "poisson", "rate": 650}, "roberta_b": {"mode": "poisson", "rate": 400}}
-
-
-def overload_doc(duration=3000, **kw):
-    d = {"profiles": "default6", "duration_ms": duration, "seed": 0, "n_gpus": 4, "concurrency_limit": 4,
-         "policy": "predictive", "goodput_window_ms": 1000, "ground_truth": dict(OVERLOAD_GT),
-         "workload": dict(OVERLOAD_WL)}
-    d.update(kw)
-    return d
-
-
-def trace_config(duration=30000):
-    doc = {"profiles": "default6", "duration_ms": duration, "seed": 2, "n_gpus": 2, "policy": "predictive",
-           "ground_truth": {"noise_sigma": 0.05}, "workload": {"yolo_v8n": {"mode": "poisson", "rate": 100}}}
-    cfg = MC.config_from_dict(doc)
-    cfg.workload.models["resnet50"] = ModelWorkload("trace", function_id="vision_gate", scale=1.0,
-                                                    trace_table=EXAMPLE_TRACE)
-    cfg.workload.models["roberta_b"] = ModelWorkload("trace", function_id="doc_reader", scale=0.5,
-                                                     trace_table=EXAMPLE_TRACE)
-    cfg.validate()
-    return cfg
-
-
-def c5_config(duration=150.0, minutes=2, seed=0, n_gpus=64):
-    """C5 shape: 20 random_profile models (m00-m05 HP bursty
-    trace, m06-m19 LP Poisson 2600/s), 64 GPUs."""
-    rng = np.random.default_rng(2604)
-    profs = {f"m{i:02d}": random_profile(rng, f"m{i:02d}", PriorityLevel.HIGH if i < 6 else PriorityLevel.LOW)
-             for i in range(20)}
-    table = {}
-    for i in range(6):
-        for m in range(minutes):
-            table.setdefault(f"hp{i}", {})[m] = float(int(rng.lognormal(math.log(150000), 0.6)))
-    wl = {f"m{i:02d}": ({"mode": "poisson", "rate": 2600}) for i in range(6, 20)}
-    doc = {"profiles": profs, "duration_ms": duration, "seed": seed, "n_gpus": n_gpus, "concurrency_limit": 4,
-           "policy": "predictive", "ground_truth": {"noise_sigma": 0.05}, "workload": wl}
-    cfg = MC.config_from_dict(doc)
-    for i in range(6):
-        cfg.workload.models[f"m{i:02d}"] = ModelWorkload("trace", function_id=f"hp{i}", scale=1.0, trace_table=table)
-    cfg.validate()
-    return cfg
+from paper_2604_28175_b200.configs import (C1, DEMO, EXAMPLE_TRACE, OVERLOAD_GT, OVERLOAD_WL,  # noqa: F401
+                                           overload_doc)
+from paper_2604_28175_b200.configs import c5 as c5_config
+from paper_2604_28175_b200.configs import trace_replay as trace_config
 
 
 def case_config(name: str):
