@@ -22,11 +22,13 @@ namespace strait {
 #define STRAIT_LIBM 1
 #endif
 #if STRAIT_LIBM
-__device__ __forceinline__ double dexp(double x) { return glibc::exp(x); }
+__device__ __forceinline__ double dexp(double x, const ulonglong2* tab = glibc::exp_table()) {
+  return glibc::exp(x, tab);
+}
 __device__ __forceinline__ double dlog(double x) { return glibc::log(x); }
 __device__ __forceinline__ double dpow(double x, double y) { return glibc::pow(x, y); }
 #else
-__device__ __forceinline__ double dexp(double x) { return ::exp(x); }
+__device__ __forceinline__ double dexp(double x, const ulonglong2* = nullptr) { return ::exp(x); }
 __device__ __forceinline__ double dlog(double x) { return ::log(x); }
 __device__ __forceinline__ double dpow(double x, double y) { return ::pow(x, y); }
 #endif
@@ -47,6 +49,7 @@ struct Pred {
   double w_cmp, w_mem;
   double coeff[2];  // [HIGH, LOW]
   double cap;
+  const ulonglong2* etab;  // exp table (global, or a kernel's shared-memory copy)
 
   __device__ __forceinline__ void load(const double* __restrict__ P, double effect_cap) {
     scale = P[0];
@@ -59,6 +62,9 @@ struct Pred {
     coeff[0] = P[5 + NM];
     coeff[1] = P[6 + NM];
     cap = effect_cap;
+#if STRAIT_LIBM
+    etab = glibc::exp_table();
+#endif
   }
 
   // predictor.py:161-176 pressure_exponent — self terms first, then metrics.
@@ -76,7 +82,7 @@ struct Pred {
       saturated = true;
       return cap;
     }
-    const double inner = scale * dexp(z) + offset;
+    const double inner = scale * dexp(z, etab) + offset;
     saturated = inner >= cap;
     if (saturated) return cap;
     return py_min(py_max(inner, 0.0), cap);

@@ -50,8 +50,11 @@ __device__ __forceinline__ double exp_special(double tmp, uint64_t sbits, uint64
 }
 
 // exp core shared by exp() and pow(): 2^(k/N) * exp(r), |r| <= ln2/2N
+// `tab` = __exp_data.tab as 128 (tail, sbits) pairs: the global copy, or a
+// shared-memory copy staged by a kernel that calls exp in its hot loop.
 template <bool POW>
-__device__ __forceinline__ double exp_core(double x, double xtail, uint64_t sign_bias, uint32_t abstop) {
+__device__ __forceinline__ double exp_core(double x, double xtail, uint64_t sign_bias, uint32_t abstop,
+                                           const ulonglong2* tab) {
   constexpr double InvLn2N = kExpInvLn2N, Shift = kExpShift;
   constexpr double NegLn2hiN = kExpNegLn2hiN, NegLn2loN = kExpNegLn2loN;
   constexpr double C2 = kExpC2, C3 = kExpC3, C4 = kExpC4, C5 = kExpC5;
@@ -62,7 +65,7 @@ __device__ __forceinline__ double exp_core(double x, double xtail, uint64_t sign
   r = __fma_rn(kd, NegLn2loN, r);         // fma
   if (POW) r = xtail + r;                 // pow's exp_inline: r += xtail
   const uint64_t top = (ki + sign_bias) << (52 - kExpBits);
-  const ulonglong2 te = __ldg(reinterpret_cast<const ulonglong2*>(kExpTab) + (ki % kN));  // one 16-B load
+  const ulonglong2 te = tab[ki % kN];  // one 16-B load
   const double tail = as_d(te.x);
   const uint64_t sbits = te.y + top;
   const double r2 = r * r;
@@ -75,8 +78,10 @@ __device__ __forceinline__ double exp_core(double x, double xtail, uint64_t sign
   return __fma_rn(tmp, scale, scale);  // fma: scale + scale * tmp
 }
 
+__device__ __forceinline__ const ulonglong2* exp_table() { return reinterpret_cast<const ulonglong2*>(kExpTab); }
+
 // math.exp (e_exp.c __exp, FMA build)
-__device__ __forceinline__ double exp(double x) {
+__device__ __forceinline__ double exp(double x, const ulonglong2* tab = exp_table()) {
   uint32_t abstop = top12(x) & 0x7ff;
   if (abstop - 0x3c9u >= 0x408u - 0x3c9u) {  // |x| < 2^-54, |x| >= 512, inf or nan
     if ((int32_t)(abstop - 0x3c9u) < 0) return 1.0 + x;
@@ -87,7 +92,7 @@ __device__ __forceinline__ double exp(double x) {
     }
     abstop = 0;  // large finite x: special-cased in the core
   }
-  return exp_core<false>(x, 0.0, 0, abstop);
+  return exp_core<false>(x, 0.0, 0, abstop, tab);
 }
 
 // math.log (e_log.c __log, FMA build)
@@ -242,7 +247,7 @@ __device__ __forceinline__ double pow(double x, double y) {
     }
     abstop = 0;
   }
-  return exp_core<true>(ehi, elo, sign_bias, abstop);
+  return exp_core<true>(ehi, elo, sign_bias, abstop, exp_table());
 }
 
 }  // namespace glibc

@@ -354,7 +354,7 @@ template <int NM>
 struct WsLayout {
   StageLayout<NM> st;
   size_t res_lat, res_intf, res_adm, cnt, stage_bytes;
-  size_t pred, full, empty, refit, copies, bytes;
+  size_t pred, full, empty, refit, copies, etab, bytes;
   __host__ __device__ WsLayout(const TileGeom& t, int nstages) : st(t) {
     res_lat = st.bytes;
     res_intf = res_lat + (size_t)t.TP * 8;
@@ -366,7 +366,8 @@ struct WsLayout {
     empty = full + 8 * kMaxStages;
     refit = empty + 8 * kMaxStages;
     copies = align_up(refit + 8 * kMaxP, 16);
-    bytes = copies + sizeof(BulkCopy) * (4 * kMaxM + 9);
+    etab = align_up(copies + sizeof(BulkCopy) * (4 * kMaxM + 9), 16);
+    bytes = etab + 128 * 16;  // shared copy of the exp table (strait_libm.cuh)
   }
 };
 
@@ -418,8 +419,13 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
   const int ncand = tg.spb * StageLayout<NM>::kCandF;
 
   BulkCopy* ctab = (BulkCopy*)(smem + W.copies);
+  ulonglong2* etab = (ulonglong2*)(smem + W.etab);
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) etab[i] = __ldg((const ulonglong2*)glibc::kExpTab + i);
   if (threadIdx.x == 0) {
     ((Pred<NM>*)(smem + W.pred))->load(a.params, a.effect_cap);
+#if STRAIT_LIBM
+    ((Pred<NM>*)(smem + W.pred))->etab = etab;
+#endif
     build_copy_table<NM, C>(a, tg, L, ctab);
     for (int s = 0; s < nstages; ++s) {
       mbar_init(&full[s], 32);  // the producer warp's cp.async arrivals; bulk bytes via expect_tx
@@ -494,7 +500,7 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
   const int pl = sl * tg.G + g;
   const int TP = tg.TP, TT = tg.TT, spb = tg.spb, G = tg.G;
   const double now = a.now;
-  const Pred<NM>& pr = *(const Pred<NM>*)(smem + W.pred);
+  const Pred<NM> pr = *(const Pred<NM>*)(smem + W.pred);  // in registers for the tile loop
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
 
   int64_t tile = blockIdx.x + (int64_t)group * gridDim.x;
