@@ -41,6 +41,14 @@ constexpr int kMaxP = STRAIT_MAX_METRICS + 7;
 __host__ __device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
 __host__ __device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
 
+// exp of the predictor's effect (a kernel may route it to a shared, non-inlined copy)
+#ifndef STRAIT_PRED_EXP
+#define STRAIT_PRED_EXP(z, tab) dexp(z, tab)
+#endif
+#ifndef STRAIT_PRED_LOG
+#define STRAIT_PRED_LOG(x) dlog(x)
+#endif
+
 // Parameters of one predictor, staged in registers/shared memory by callers.
 template <int NM>
 struct Pred {
@@ -53,7 +61,7 @@ struct Pred {
 
   __device__ __forceinline__ void load(const double* __restrict__ P, double effect_cap) {
     scale = P[0];
-    log_base = dlog(P[1]);
+    log_base = STRAIT_PRED_LOG(P[1]);
     offset = P[2];
 #pragma unroll
     for (int i = 0; i < NM; ++i) w[i] = P[3 + i];
@@ -82,7 +90,7 @@ struct Pred {
       saturated = true;
       return cap;
     }
-    const double inner = scale * dexp(z, etab) + offset;
+    const double inner = scale * STRAIT_PRED_EXP(z, etab) + offset;
     saturated = inner >= cap;
     if (saturated) return cap;
     return py_min(py_max(inner, 0.0), cap);

@@ -38,10 +38,29 @@
 
 #include "../../include/strait_replay.h"
 #include "strait_capi.cuh"
+
+// The engine's hot loop is large and every warp sits at a different point of
+// it, so instruction-cache footprint matters more than call overhead: exp,
+// log and pow get ONE out-of-line copy each per translation unit.
+namespace strait {
+namespace rp {
+static __device__ __noinline__ double rp_exp(double x);
+static __device__ __noinline__ double rp_log(double x);
+static __device__ __noinline__ double rp_pow(double x, double y);
+}  // namespace rp
+}  // namespace strait
+#define STRAIT_PRED_EXP(z, tab) ::strait::rp::rp_exp(z)
+#define STRAIT_PRED_LOG(x) ::strait::rp::rp_log(x)
 #include "strait_device.cuh"
 
 namespace strait {
 namespace rp {
+
+static __device__ __noinline__ double rp_exp(double x) { return dexp(x); }
+static __device__ __noinline__ double rp_log(double x) { return dlog(x); }
+static __device__ __noinline__ double rp_pow(double x, double y) { return dpow(x, y); }
+// IEEE binary64 division (same result as `a / b`; one out-of-line copy)
+static __device__ __noinline__ double rp_div(double a, double b) { return __ddiv_rn(a, b); }
 
 constexpr int kKC = 0, kTC = 1, kARR = 2, kTO = 3, kTICK = 4;  // simulation.py:28-33 tie ranks
 constexpr double kWorkEps = 1e-9;                               // simulation.py:35
@@ -223,7 +242,7 @@ struct Sim {
     }
     const double d = end - SD(SD_TL, s);
 #pragma unroll
-    for (int i = 0; i < NM; ++i) out[i] = (SD(SD_ACC + i, s) + SD(SD_VL + i, s) * d) / total;
+    for (int i = 0; i < NM; ++i) out[i] = rp_div(SD(SD_ACC + i, s) + SD(SD_VL + i, s) * d, total);
   }
 
   // ------------------------------------------------------------ runtime (runtime.py:104-141)
@@ -233,6 +252,7 @@ struct Sim {
     if (lane < NM) {
       double a = 0.0, lp = 0.0;
       const int n = GI(GI_NRUN, g);
+#pragma unroll 1
       for (int p = 0; p < n; ++p) {
         const int s = slot_at(g, p);
         const double c = SD(SD_CON + lane, s);
@@ -266,7 +286,7 @@ struct Sim {
     double x = cf->gt_w_cmp * SD(SD_CMP, s) + cf->gt_w_mem * SD(SD_MEM, s);
 #pragma unroll
     for (int i = 0; i < NM; ++i) x += cf->gt_w[i] * SD(SD_AEX + i, s);
-    double effect = cf->gt_family == 0 ? cf->gt_scale * dpow(cf->gt_base, x) + cf->gt_offset
+    double effect = cf->gt_family == 0 ? cf->gt_scale * rp_pow(cf->gt_base, x) + cf->gt_offset
                                        : cf->gt_scale * x * x + cf->gt_offset;
     effect = py_max(0.0, effect);
     return 1.0 + effect * (SB(SB_PRIO, s) == 0 ? cf->gt_pf_high : cf->gt_pf_low) * SD(SD_NOISE, s);
@@ -278,8 +298,9 @@ struct Sim {
     bool ok = !(d < 0);
     if (d > 0) {
       const double slow = SD(SD_SLOW, s);
-      SD(SD_WORK, s) = SD(SD_WORK, s) + d / slow;
-      double rem = SD(SD_REM, s) - d / slow;
+      const double q = rp_div(d, slow);  // the reference divides twice; same value
+      SD(SD_WORK, s) = SD(SD_WORK, s) + q;
+      double rem = SD(SD_REM, s) - q;
       if (rem < -kWorkEps) ok = false;
       if (rem < 0.0) rem = 0.0;
       SD(SD_REM, s) = rem;
@@ -350,7 +371,7 @@ struct Sim {
       saturated = true;
       inner = __longlong_as_double(0x7ff0000000000000LL);
     } else {
-      pow_bx = dexp(z);
+      pow_bx = rp_exp(z);
       inner = pr.scale * pow_bx + pr.offset;
       saturated = inner >= cap;
     }
@@ -364,7 +385,7 @@ struct Sim {
       const double log_b = pr.log_base;
       const double zz = pr.scale * pow_bx;
       if (lane == 0) d = pow_bx * cfc;
-      else if (lane == 1) d = pr.scale * x * dexp((x - 1.0) * log_b) * cfc;
+      else if (lane == 1) d = pr.scale * x * rp_exp((x - 1.0) * log_b) * cfc;
       else if (lane == 2) d = cfc;
       else if (lane < 3 + NM) {
         double ai = 0.0;
@@ -391,9 +412,9 @@ struct Sim {
     if (owner && lane != other) {
       adam_m = b1 * adam_m + (1.0 - b1) * gk;
       adam_v = b2 * adam_v + (1.0 - b2) * gk * gk;
-      const double m_hat = adam_m / bc1;
-      const double v_hat = adam_v / bc2;
-      p -= cf->learning_rate * m_hat / (sqrt(v_hat) + cf->eps);
+      const double m_hat = rp_div(adam_m, bc1);
+      const double v_hat = rp_div(adam_v, bc2);
+      p -= rp_div(cf->learning_rate * m_hat, sqrt(v_hat) + cf->eps);
       if (lane == 0) p = py_max(p, 1e-6);        // enforce_floors (predictor.py:98-102)
       if (lane == 1) p = py_max(p, 1.0 + 1e-6);
     }
@@ -441,7 +462,7 @@ struct Sim {
   // check_violate (scheduler.py:118-161) of the candidate on GPU g; lane-local.
   __device__ __forceinline__ bool violate(int g, const Cand& cd, int cprio, double now) const {
     if (cprio == 1) {  // LOW: LP aggregate + contribution vs the AIMD cap (:130-135)
-      const double capf = GD(GD_CAP, g) / 100.0;
+      const double capf = rp_div(GD(GD_CAP, g), 100.0);
 #pragma unroll
       for (int i = 0; i < NM; ++i)
         if (GD(GD_LPA + i, g) + cd.c[i] > capf) return true;
@@ -459,7 +480,7 @@ struct Sim {
       const double ks = SD(SD_KS, s), tk = SD(SD_TK, s);
       const double elapsed = py_max(0.0, now - ks);
       const double denom = intf_cur * tk;
-      const double progress = denom > 0 ? py_min(1.0, elapsed / denom) : 1.0;
+      const double progress = denom > 0 ? py_min(1.0, rp_div(elapsed, denom)) : 1.0;
       const double remaining = (1.0 - progress) * tk * intf_new;
       const double projected = py_max(now, ks) + remaining;
       if (projected > SD(SD_DL, s)) return true;
@@ -733,6 +754,7 @@ struct Sim {
       const bool rdy = km != kNoKey;
       if (rdy) {
         int rank = 0;
+#pragma unroll 1
         for (int j = 0; j < M; ++j) {
           const unsigned long long kj = qk[j];
           rank += kj < km || (kj == km && j < m);
@@ -797,6 +819,7 @@ struct Sim {
         const double off = now - predicted;
         if (off != 0.0) {
           GD(GD_TAV, g) = GD(GD_TAV, g) + off;
+#pragma unroll 1
           for (int i = 0; i < npn; ++i) GD(GD_PEND + (nph + i) % C, g) = GD(GD_PEND + (nph + i) % C, g) + off;
         }
       }
@@ -848,7 +871,7 @@ struct Sim {
     double tw[NM];
     tl_twa(s, now, tw);
     const double tk = tab_kernel(m, k);
-    const double actual = measured / tk;
+    const double actual = rp_div(measured, tk);
     if (!(actual > 0)) fail(STRAIT_EINVAL);
     // GpuRuntimeState.remove_entry (runtime.py:132-141): shift the running list
     const int n = GI(GI_NRUN, g);
@@ -896,7 +919,7 @@ struct Sim {
       if (g < NG) {
         const double old = GD(GD_CAP, g), last = GD(GD_TICK, g);
         if (now < last) bad = true;
-        const double whole = floor((now - last) / cf->aimd_interval);
+        const double whole = floor(rp_div(now - last, cf->aimd_interval));
         cap = old;
         if (whole > 0) {
           cap = py_min(cf->aimd_ceiling, old + whole * cf->aimd_increase);
@@ -952,6 +975,7 @@ struct Sim {
       hp_arr += __shfl_xor_sync(kFull, hp_arr, off);
       lp_arr += __shfl_xor_sync(kFull, lp_arr, off);
     }
+#pragma unroll 1
     for (int64_t i = lane; i < N; i += 32) A->req_status[base + i] = 0;
     for (int g = lane; g < NG; g += 32) cap_row_at(g, 0.0, g, cf->aimd_floor);  // simulation.py:196-197
     sync();
@@ -971,6 +995,7 @@ struct Sim {
       double bt = INF;
       unsigned long long bk = kNoKey;
       int bi = -1;
+#pragma unroll 1
       for (int i = lane; i < NE; i += 32) {
         const double t = ed[i];
         const unsigned long long kk = ek[i];
