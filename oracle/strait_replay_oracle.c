@@ -161,6 +161,8 @@ typedef struct {
   int64_t *front_gen, *timeout_gen;
   double P[MAXP], Mv[MAXP], Vv[MAXP];
   int64_t step;
+  int lp_allowance;   /* ReactiveState (baselines.py:81-110) */
+  double last_reset;
   int err;
   int64_t *cnt;
 } Sim;
@@ -340,7 +342,28 @@ static int64_t q_len(const Sim *S, int m) { return S->q_tail[m] - S->q_head[m]; 
 static double req_arr(const Sim *S, int64_t gi) { return S->A->arr_time[gi]; }
 static double req_deadline(const Sim *S, int m, int64_t gi) { return req_arr(S, gi) + S->A->models.deadline[m]; }
 
+/* ReactiveState.catch_up (baselines.py:99-104) */
+static void reactive_catch_up(Sim *S, double now) {
+  const double period = S->cfg->reactive_period;
+  if (now - S->last_reset >= period) {
+    double periods = floor((now - S->last_reset) / period);
+    S->lp_allowance = S->cfg->reactive_default;
+    S->last_reset += periods * period;
+  }
+}
+
 static void signal_hp_violation(Sim *S, int gpu_id, double now) { /* simulation.py:223-229 */
+  if (S->cfg->policy != STRAIT_POLICY_PREDICTIVE) {
+    /* baselines: TemporalPolicy / StaticSpatialPolicy inherit the no-op
+     * on_hp_violation (scheduler.py:225-226); ReactiveSpatialPolicy shrinks the
+     * LP allowance (baselines.py:131-133, 106-107).  AIMD caps never change. */
+    if (S->cfg->policy == STRAIT_POLICY_REACTIVE) {
+      reactive_catch_up(S, now);
+      int a = S->lp_allowance - 1;
+      S->lp_allowance = a > S->cfg->reactive_min ? a : S->cfg->reactive_min;
+    }
+    return;
+  }
   for (int g = 0; g < S->cfg->n_gpus; ++g) {
     if (gpu_id >= 0 && g != gpu_id) continue;
     double old = S->gpus[g].cap_pct;
@@ -449,7 +472,54 @@ static Plan best_for(Sim *S, int m, int k, double front, double now) {
   return best;
 }
 
+/* _isolated_latency_plan (baselines.py:34-37): est = (now - front) + total(size), intf 1.0 */
+static Plan isolated_plan(Sim *S, int m, int gpu, int size, double now) {
+  double front = req_arr(S, S->q_store[S->q_head[m]]);
+  Plan p = {size, gpu, (now - front) + MTAB(total, m, size), 1.0};
+  return p;
+}
+
+/* the baselines' propose (baselines.py:40-128); returns size in .ok, 0 = None */
+static Plan propose_baseline(Sim *S, int m, double now) {
+  Plan none = {0, -1, 0, 0};
+  const int G = S->cfg->n_gpus, pol = S->cfg->policy;
+  int64_t len = q_len(S, m);
+  int kmax = (int)(len < S->A->models.max_batch[m] ? len : S->A->models.max_batch[m]);
+  if (pol == STRAIT_POLICY_TEMPORAL) { /* first idle GPU, largest isolated-feasible size */
+    int idle = -1;
+    for (int g = 0; g < G && idle < 0; ++g)
+      if (S->gpus[g].n_running == 0) idle = g;
+    if (idle < 0) return none;
+    double deadline = req_deadline(S, m, S->q_store[S->q_head[m]]);
+    int lo = 1, hi = kmax, best = 0;
+    while (lo <= hi) {
+      int mid = (lo + hi) / 2;
+      if (now + MTAB(total, m, mid) <= deadline) best = mid, lo = mid + 1;
+      else hi = mid - 1;
+    }
+    return best ? isolated_plan(S, m, idle, best, now) : none;
+  }
+  /* static / reactive: min (len(running), gpu_id) over the open GPUs; size = everything buffered */
+  int prio = S->A->models.prio[m];
+  int bound = prio == 1 ? S->lp_allowance : S->cfg->reactive_hp_bound;
+  int cap = S->cfg->static_cap < S->cfg->concurrency_limit ? S->cfg->static_cap : S->cfg->concurrency_limit;
+  int best = -1;
+  for (int g = 0; g < G; ++g) {
+    const Gpu *gp = &S->gpus[g];
+    int open;
+    if (pol == STRAIT_POLICY_STATIC) open = gp->n_running < cap;
+    else {
+      int count = 0;
+      for (int j = 0; j < gp->n_running; ++j) count += S->ent[gp->running[j]].prio == prio;
+      open = gp->n_running < S->cfg->concurrency_limit && count < bound;
+    }
+    if (open && (best < 0 || gp->n_running < S->gpus[best].n_running)) best = g;
+  }
+  return best < 0 ? none : isolated_plan(S, m, best, kmax, now);
+}
+
 static Plan propose(Sim *S, int m, double now) { /* scheduler.py:257-285 */
+  if (S->cfg->policy != STRAIT_POLICY_PREDICTIVE) return propose_baseline(S, m, now);
   double front = req_arr(S, S->q_store[S->q_head[m]]);
   int64_t len = q_len(S, m);
   int kmax = (int)(len < S->A->models.max_batch[m] ? len : S->A->models.max_batch[m]);
@@ -521,6 +591,7 @@ static void ensure_timeout(Sim *S, int m, double now) { /* simulation.py:231-238
 static void do_pass(Sim *S, double now) { /* simulation.py:301-361 + scheduler.py:355-378 */
   int64_t pass_id = ++S->pass_seq;
   S->cnt[STRAIT_RC_PASSES]++;
+  if (S->cfg->policy == STRAIT_POLICY_REACTIVE) reactive_catch_up(S, now); /* begin_pass */
   int order[256], n = 0;
   for (int m = 0; m < S->M; ++m)
     if (q_len(S, m)) order[n++] = m;
@@ -673,6 +744,8 @@ static int run_one(const StraitReplayArgs *A, int64_t r) {
   memcpy(S->Mv, st + S->np, S->np * sizeof(double));
   memcpy(S->Vv, st + 2 * S->np, S->np * sizeof(double));
   S->step = A->pred_step[r];
+  S->lp_allowance = S->cfg->reactive_default;
+  S->last_reset = 0.0;
   int G = S->cfg->n_gpus;
   S->gpus = calloc(G, sizeof(Gpu));
   for (int g = 0; g < G; ++g) S->gpus[g].cap_pct = S->cfg->aimd_floor;

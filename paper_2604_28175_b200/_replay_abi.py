@@ -21,14 +21,17 @@ class ReplayModels(C.Structure):
 class ReplayConfig(C.Structure):
     _fields_ = [("n_gpus", C.c_int32), ("concurrency_limit", C.c_int32), ("use_priority_order", C.c_int32),
                 ("use_meet", C.c_int32), ("use_violate", C.c_int32), ("gt_family", C.c_int32),
-                ("has_noise", C.c_int32), ("pad", C.c_int32),
+                ("has_noise", C.c_int32), ("policy", C.c_int32),
                 ("effect_cap", C.c_double), ("learning_rate", C.c_double), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("eps", C.c_double), ("huber_delta", C.c_double),
                 ("gt_scale", C.c_double), ("gt_base", C.c_double), ("gt_offset", C.c_double),
                 ("gt_w_cmp", C.c_double), ("gt_w_mem", C.c_double), ("gt_pf_high", C.c_double),
                 ("gt_pf_low", C.c_double), ("gt_w", C.c_double * MAX_METRICS),
                 ("aimd_floor", C.c_double), ("aimd_ceiling", C.c_double), ("aimd_increase", C.c_double),
-                ("aimd_interval", C.c_double)]
+                ("aimd_interval", C.c_double), ("static_cap", C.c_int32), ("reactive_default", C.c_int32),
+                ("reactive_min", C.c_int32), ("reactive_hp_bound", C.c_int32), ("reactive_period", C.c_double)]
+
+POLICY_CODES = {"predictive": 0, "temporal": 1, "static": 2, "reactive": 3}
 
 
 ARG_ARRAYS = ["cfg", "req_off", "arr_time", "arr_model", "model_req", "mr_off", "noise", "bc1", "bc2",

@@ -141,6 +141,8 @@ struct Sim {
   int64_t step;
   unsigned long long seq;
   int batch_seq, pass_seq, done_order, err;
+  int lp_allowance;   // ReactiveState (baselines.py:81-110)
+  double last_reset;
   int64_t next_arr, resolved;
   int64_t c_batches, c_completed, c_passes, c_cap_rows, c_events, c_hp_viol, c_lp_viol, c_hp_drop, c_lp_drop;
 
@@ -338,8 +340,28 @@ struct Sim {
     fail_any(!ok, STRAIT_EORDER);
   }
 
-  // _signal_hp_violation (simulation.py:223-229) -> AimdState.reset (runtime.py:36-37)
+  // ReactiveState.catch_up (baselines.py:99-104)
+  __device__ __forceinline__ void reactive_catch_up(double now) {
+    const double period = cf->reactive_period;
+    if (now - last_reset >= period) {
+      const double periods = floor(rp_div(now - last_reset, period));
+      lp_allowance = cf->reactive_default;
+      last_reset += periods * period;
+    }
+  }
+
+  // _signal_hp_violation (simulation.py:223-229) -> policy.on_hp_violation:
+  // AimdState.reset for the predictive policy (scheduler.py:287-292), the
+  // reactive allowance for ReactiveSpatialPolicy (baselines.py:131-133), a
+  // no-op for the other baselines (scheduler.py:225-226).
   __device__ __forceinline__ void signal_hp(int gpu_id, double now) {
+    if (cf->policy != STRAIT_POLICY_PREDICTIVE) {
+      if (cf->policy == STRAIT_POLICY_REACTIVE) {
+        reactive_catch_up(now);
+        lp_allowance = max(cf->reactive_min, lp_allowance - 1);
+      }
+      return;
+    }
     for (int g0 = 0; g0 < NG; g0 += 32) {
       const int g = g0 + lane;
       bool changed = false;
@@ -544,6 +566,57 @@ struct Sim {
     return warp_best(found, bg, bl, bi);
   }
 
+  // The baselines' propose (baselines.py:34-128): placement by occupancy only,
+  // BatchPlan(est = (now - front) + total(size), intf = 1.0).
+  __device__ __forceinline__ int propose_baseline(int m, double now, Plan& plan) const {
+    const double front = front_arrival(m);
+    const int kmax = min(q_len(m), mmaxb(m));
+    const int pol = cf->policy;
+    int gpu = -1, size = kmax;
+    if (pol == STRAIT_POLICY_TEMPORAL) {  // first idle GPU; largest size meeting the front deadline
+      for (int g0 = 0; g0 < NG && gpu < 0; g0 += 32) {
+        const unsigned idle = __ballot_sync(kFull, g0 + lane < NG && GI(GI_NRUN, g0 + lane) == 0);
+        if (idle) gpu = g0 + __ffs(idle) - 1;
+      }
+      if (gpu < 0) return 0;
+      const double deadline = front + mdeadline(m);
+      int lo = 1, hi = kmax;
+      size = 0;
+      while (lo <= hi) {
+        const int mid = (lo + hi) / 2;
+        if (now + tab_total(m, mid) <= deadline) size = mid, lo = mid + 1;
+        else hi = mid - 1;
+      }
+      if (!size) return 0;
+    } else {  // static / reactive: min (len(running), gpu_id) over the open GPUs
+      const int prio = mprio(m);
+      const int bound = prio == 1 ? lp_allowance : cf->reactive_hp_bound;
+      const int cap = min(cf->static_cap, CONC);
+      unsigned best = ~0u;
+      for (int g0 = 0; g0 < NG; g0 += 32) {
+        const int g = g0 + lane;
+        unsigned key = ~0u;
+        if (g < NG) {
+          const int n = GI(GI_NRUN, g);
+          bool open;
+          if (pol == STRAIT_POLICY_STATIC) {
+            open = n < cap;
+          } else {
+            int count = 0;
+            for (int p = 0; p < n; ++p) count += SB(SB_PRIO, slot_at(g, p)) == prio;
+            open = n < CONC && count < bound;
+          }
+          if (open) key = ((unsigned)n << 16) | (unsigned)g;
+        }
+        best = min(best, __reduce_min_sync(kFull, key));
+      }
+      if (best == ~0u) return 0;
+      gpu = (int)(best & 0xffffu);
+    }
+    plan = Plan{true, gpu, (now - front) + tab_total(m, size), 1.0};
+    return size;
+  }
+
   // PredictivePolicy.propose (scheduler.py:257-285) + largest_feasible (:78-90).
   // When every size fits in the warp (kmax segments of W = pow2ceil(n_gpus)
   // lanes), all sizes are evaluated at once (lane = (k - 1) * W + g; best_for
@@ -734,6 +807,8 @@ struct Sim {
   __device__ __forceinline__ void do_pass(double now) {
     const int pass_id = ++pass_seq;
     ++c_passes;
+    const bool predictive = cf->policy == STRAIT_POLICY_PREDICTIVE;
+    if (cf->policy == STRAIT_POLICY_REACTIVE) reactive_catch_up(now);  // begin_pass (baselines.py:113-114)
     // queue_order (scheduler.py:249-255): stable sort of the ready queues by
     // (priority, front arrival, model_id), as a lane-parallel rank sort.
     // key = priority in the top bit | bit pattern of the (>= 0) front arrival;
@@ -771,15 +846,15 @@ struct Sim {
       const int len = q_len(m);
       if (!len) continue;
       if (!(len >= mmaxb(m) || now >= front_arrival(m) + mtimeout(m))) continue;  // TaskQueue.eligible
-      if (!icur_ready) {
+      if (predictive && !icur_ready) {
         icur_all(now);
         icur_ready = true;
       }
       Plan plan;
-      const int k = propose(m, now, plan);
+      const int k = predictive ? propose(m, now, plan) : propose_baseline(m, now, plan);
       if (!k) continue;
       submit(m, k, plan, now, pass_id);
-      icur_gpu(plan.gpu, now);
+      if (predictive) icur_gpu(plan.gpu, now);
     }
     // _ensure_timeout for every queue in model order (simulation.py:360-361)
     for (int m0 = 0; m0 < M; m0 += 32) {
@@ -1133,6 +1208,8 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   S.go = (int8_t*)(base + L.go);
   S.qb = (int8_t*)(base + L.qb);
   S.batch_seq = S.pass_seq = S.done_order = S.err = 0;
+  S.lp_allowance = S.cf->reactive_default;
+  S.last_reset = 0.0;
   S.resolved = 0;
   S.c_batches = S.c_completed = S.c_passes = S.c_events = 0;
   S.c_hp_viol = S.c_lp_viol = S.c_hp_drop = S.c_lp_drop = 0;

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from . import _device as D
-from ._replay_abi import ARG_ARRAYS, RC, RC_N, ReplayArgs, ReplayConfig, ReplayModels
+from ._replay_abi import ARG_ARRAYS, POLICY_CODES, RC, RC_N, ReplayArgs, ReplayConfig, ReplayModels
 from .config import ExperimentConfig
 from .domain import PriorityLevel
 from .predictor import InterferencePredictor, PredictorParams, bias_correction_tables
@@ -80,16 +80,29 @@ def model_tables(profiles: dict) -> dict:
     return dict(ids=ids, M=M, nm=nm, B=B, **t)
 
 
+# baselines.py defaults: StaticSpatialPolicy(cap=3), ReactiveState() (lines 62-110)
+STATIC_CAP = 3
+REACTIVE = dict(default=3, min=1, hp_bound=3, period=200.0)
+
+
 def replay_config(cfg: ExperimentConfig, pred: InterferencePredictor) -> ReplayConfig:
-    if cfg.policy != "predictive":
-        raise NotImplementedError(f"device replay implements the predictive policy, got {cfg.policy!r}")
+    if cfg.policy not in POLICY_CODES:
+        raise ValueError(f"unknown policy {cfg.policy!r}, expected one of {tuple(POLICY_CODES)}")
     variant = cfg.policy_variant
-    gt = cfg.ground_truth.without_priority_advantage() if variant == "no_gamma_advantage" else cfg.ground_truth
+    predictive = cfg.policy == "predictive"
+    # simulation.py:160-161: the no_gamma_advantage ablation only applies to the predictive policy
+    gt = (cfg.ground_truth.without_priority_advantage() if predictive and variant == "no_gamma_advantage"
+          else cfg.ground_truth)
     c = ReplayConfig()
     c.n_gpus, c.concurrency_limit = cfg.n_gpus, cfg.concurrency_limit
-    c.use_priority_order = int(variant != "no_priority_scan")
+    c.policy = POLICY_CODES[cfg.policy]
+    # the baselines scan queues in the base priority order (scheduler.py:214-217)
+    c.use_priority_order = int(not predictive or variant != "no_priority_scan")
     c.use_meet = int(variant != "no_meet")
     c.use_violate = int(variant != "no_violate_aimd")
+    c.static_cap = STATIC_CAP
+    c.reactive_default, c.reactive_min = REACTIVE["default"], REACTIVE["min"]
+    c.reactive_hp_bound, c.reactive_period = REACTIVE["hp_bound"], REACTIVE["period"]
     c.gt_family = 0 if gt.family == "exponential" else 1
     c.has_noise = int(gt.noise_sigma > 0)
     c.effect_cap = pred.params.effect_cap

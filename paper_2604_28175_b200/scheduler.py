@@ -13,6 +13,7 @@ reference's own data structures; every prediction, violate/meet check and the
 """
 from __future__ import annotations
 
+import math
 from collections import deque
 from dataclasses import dataclass
 from typing import Callable, Iterable, Optional, Sequence
@@ -347,14 +348,114 @@ def run_scheduling_pass(policy: SchedulingPolicy, queues: Iterable[TaskQueue], g
     return decisions
 
 
+def _isolated_latency_plan(queue: TaskQueue, gpu_id: int, size: int, now: float) -> BatchPlan:
+    """baselines.py:34-37."""
+    latency = (now - queue.front().arrival_time) + queue.profile.total_latency_ms(size)
+    return BatchPlan(size=size, gpu_id=gpu_id, est_latency=latency, intf_pred=1.0, assumed=())
+
+
+class TemporalPolicy(SchedulingPolicy):
+    """baselines.py:40-59: one batch per GPU; largest size meeting the front deadline in isolation."""
+
+    name = "temporal"
+
+    def propose(self, queue, gpus, now):
+        idle = [g for g in gpus if not g.running]
+        if not idle:
+            return None
+        profile = queue.profile
+        deadline = queue.front().deadline_abs
+        k_max = min(len(queue.pending), profile.max_batch_size)
+        size = largest_feasible(k_max, lambda k: now + profile.total_latency_ms(k) <= deadline)
+        return None if size is None else _isolated_latency_plan(queue, idle[0].gpu_id, size, now)
+
+
+class StaticSpatialPolicy(SchedulingPolicy):
+    """baselines.py:62-78: fixed concurrency cap, least-loaded GPU, everything buffered."""
+
+    name = "static"
+
+    def __init__(self, cap: int = 3):
+        self.cap = cap
+
+    def propose(self, queue, gpus, now):
+        open_gpus = [g for g in gpus if len(g.running) < min(self.cap, g.concurrency_limit)]
+        if not open_gpus:
+            return None
+        gpu = min(open_gpus, key=lambda g: (len(g.running), g.gpu_id))
+        return _isolated_latency_plan(queue, gpu.gpu_id, min(len(queue.pending), queue.profile.max_batch_size), now)
+
+
+@dataclass
+class ReactiveState:
+    """baselines.py:81-107."""
+
+    lp_allowance: int = 3
+    default_allowance: int = 3
+    min_allowance: int = 1
+    hp_bound: int = 3
+    reset_period_ms: float = 200.0
+    last_reset: float = 0.0
+
+    def catch_up(self, now: float) -> None:
+        if now - self.last_reset >= self.reset_period_ms:
+            periods = math.floor((now - self.last_reset) / self.reset_period_ms)
+            self.lp_allowance = self.default_allowance
+            self.last_reset += periods * self.reset_period_ms
+
+    def on_hp_violation(self) -> None:
+        self.lp_allowance = max(self.min_allowance, self.lp_allowance - 1)
+
+
+class ReactiveSpatialPolicy(SchedulingPolicy):
+    """baselines.py:110-133: LP concurrency throttled by HP deadline misses."""
+
+    name = "reactive"
+
+    def __init__(self, state: Optional[ReactiveState] = None):
+        self.state = state if state is not None else ReactiveState()
+
+    def begin_pass(self, now: float) -> None:
+        self.state.catch_up(now)
+
+    def _class_open(self, gpu: GpuRuntimeState, priority: PriorityLevel) -> bool:
+        if not gpu.has_slot():
+            return False
+        count = sum(1 for e in gpu.running if e.priority is priority)
+        bound = self.state.lp_allowance if priority is PriorityLevel.LOW else self.state.hp_bound
+        return count < bound
+
+    def propose(self, queue, gpus, now):
+        open_gpus = [g for g in gpus if self._class_open(g, queue.priority)]
+        if not open_gpus:
+            return None
+        gpu = min(open_gpus, key=lambda g: (len(g.running), g.gpu_id))
+        return _isolated_latency_plan(queue, gpu.gpu_id, min(len(queue.pending), queue.profile.max_batch_size), now)
+
+    def on_hp_violation(self, gpus, gpu_id, now):
+        self.state.catch_up(now)
+        self.state.on_hp_violation()
+
+
+POLICY_NAMES = ("predictive", "temporal", "static", "reactive")
+ABLATION_VARIANTS = ("full", "no_priority_scan", "no_gamma_advantage", "no_meet", "no_violate_aimd")
+
+
 def make_policy(name: str, predictor: Optional[InterferencePredictor] = None, variant: str = "full"):
-    """baselines.py:136-160 registry, restricted to the north-star policy."""
-    if name != "predictive":
-        raise NotImplementedError(f"policy {name!r}: the B200 path implements the predictive policy")
-    if predictor is None:
-        raise ValueError("predictive policy needs a predictor")
-    variants = {"full": {}, "no_priority_scan": dict(use_priority_order=False), "no_meet": dict(use_meet=False),
-                "no_violate_aimd": dict(use_violate=False), "no_gamma_advantage": {}}
-    if variant not in variants:
-        raise ValueError(f"unknown ablation variant {variant!r}")
-    return PredictivePolicy(predictor, **variants[variant])
+    """baselines.py:136-160 registry.  Whole replays of every policy run on the
+    device (simulation.run / replay.ReplayBatch); these objects serve the
+    per-call pass API (run_scheduling_pass)."""
+    if name == "predictive":
+        if variant not in ABLATION_VARIANTS:
+            raise ValueError(f"unknown ablation variant {variant!r}")
+        if predictor is None:
+            raise ValueError("predictive policy needs a predictor")
+        return PredictivePolicy(predictor, use_priority_order=variant != "no_priority_scan",
+                                use_meet=variant != "no_meet", use_violate=variant != "no_violate_aimd")
+    if name == "temporal":
+        return TemporalPolicy()
+    if name == "static":
+        return StaticSpatialPolicy()
+    if name == "reactive":
+        return ReactiveSpatialPolicy()
+    raise ValueError(f"unknown policy {name!r}, expected one of {POLICY_NAMES}")

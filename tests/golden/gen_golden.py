@@ -4,6 +4,7 @@ inputs.  The fixtures pin the CPU oracle (oracle/) and the CUDA path.
 
     python tests/golden/gen_golden.py            # all fixtures
     python tests/golden/gen_golden.py replay     # only the replay fixtures
+    python tests/golden/gen_golden.py replay ov_static ...   # selected replay cases
 
 Run in the build container (the reference does not exist on the GPU box;
 the committed .npz files travel instead).
@@ -324,6 +325,11 @@ REPLAY_CASES = {
                                                                  offset=-0.4)), None),
     "ov_nonoise_2gpu": ("doc", overload_doc(400, n_gpus=2, ground_truth=dict(OVERLOAD_GT, noise_sigma=0.0)), None),
     "c5_slice": ("doc", None, "c5"),
+    # baseline policies behind the same pass seam (baselines.py:40-133)
+    "ov_temporal": ("doc", overload_doc(500, policy="temporal"), None),
+    "ov_static": ("doc", overload_doc(500, policy="static"), None),
+    "ov_reactive": ("doc", overload_doc(1500, policy="reactive"), None),
+    "c1_reactive": ("doc", dict(C1_DOC, duration_ms=5000, policy="reactive"), None),
 }
 
 
@@ -417,12 +423,12 @@ def reference_replay_arrays(name, tmpdir):
     return out
 
 
-def gen_replay():
+def gen_replay(names=None):
     import tempfile
     import yaml
     os.makedirs(os.path.join(HERE, "replay"), exist_ok=True)
     with tempfile.TemporaryDirectory() as tmp:
-        for name in REPLAY_CASES:
+        for name in names or REPLAY_CASES:
             arrays = reference_replay_arrays(name, tmp)
             doc, _ = replay_case_docs(name, tmp)
             np.savez_compressed(os.path.join(HERE, "replay", f"{name}.npz"), **arrays)
@@ -432,6 +438,9 @@ def gen_replay():
 
 if __name__ == "__main__":
     what = sys.argv[1:] or ["predict", "latency", "refit", "sweep", "twa", "replay"]
+    if what[0] == "replay" and len(what) > 1:  # gen_golden.py replay <case> ...
+        gen_replay(what[1:])
+        sys.exit(0)
     for w in what:
         print("generating", w, flush=True)
         globals()[f"gen_{w}"]()

@@ -29,13 +29,19 @@ def case_config(name: str):
                 "ov_quadratic": dict(ground_truth=dict(OVERLOAD_GT, family="quadratic", scale=0.3, offset=-0.4))}
     if name in variants:
         return MC.config_from_dict(overload_doc(500, **variants[name]))
+    if name in ("ov_temporal", "ov_static"):
+        return MC.config_from_dict(overload_doc(500, policy=name[3:]))
+    if name == "ov_reactive":
+        return MC.config_from_dict(overload_doc(1500, policy="reactive"))
+    if name == "c1_reactive":
+        return MC.config_from_dict(dict(C1, duration_ms=5000, policy="reactive"))
     if name == "ov_nonoise_2gpu":
         return MC.config_from_dict(overload_doc(400, n_gpus=2, ground_truth=dict(OVERLOAD_GT, noise_sigma=0.0)))
     raise KeyError(name)
 
 
 CASES = ["demo", "c1", "overload", "trace", "ov_no_meet", "ov_no_violate", "ov_no_prio", "ov_no_gamma",
-         "ov_quadratic", "ov_nonoise_2gpu", "c5_slice"]
+         "ov_quadratic", "ov_nonoise_2gpu", "c5_slice", "ov_temporal", "ov_static", "ov_reactive", "c1_reactive"]
 
 # arrays compared bit-exactly between the reference, the C oracle and (decisions) the device
 REQ_KEYS = ("req_status", "req_violated", "req_batch")
