@@ -1,0 +1,75 @@
+"""GPU: the reference's end-to-end acceptance criteria (pkg/tests/test_acceptance.py,
+SPEC.md:615-627) on the device replay engine — all 4 policies x 5 seeds of the
+overload workload plus the ablation in ONE strait_replay launch:
+
+* c09 (test_acceptance.py:359-378): predictive cuts HP violations by >= 1 pp
+  against every baseline without giving up more than 5 pp LP, on >= 4/5 seeds;
+* c10 (:381-390): removing the violation check and the adaptive cap at least
+  doubles HP misses;
+* c12 (:441-445): identical inputs give identical replays;
+* c13 (:448-463): work conservation over > 10,000 batches;
+and every replay equals the C oracle's (decisions, outcomes, counts)."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+POLICIES = ("predictive", "temporal", "static", "reactive")
+SEEDS = (0, 1, 2, 3, 4)
+
+
+def _specs():
+    from paper_2604_28175_b200.configs import overload
+    from paper_2604_28175_b200.replay import ReplaySpec
+
+    specs = [ReplaySpec(overload(3000.0, policy=p), s) for p in POLICIES for s in SEEDS]
+    specs.append(ReplaySpec(overload(3000.0, policy_variant="no_violate_aimd"), 0))
+    return specs
+
+
+def _rates(res, r):
+    hp, lp = res.violation_rates(r)
+    return hp, lp
+
+
+def test_acceptance_c09_c10_c12_c13_on_device(cuda, oracle):
+    from paper_2604_28175_b200.replay import ReplayBatch
+
+    batch = ReplayBatch(_specs())
+    res = batch.run()
+    res.check()
+    idx = {(p, s): i for i, (p, s) in enumerate((p, s) for p in POLICIES for s in SEEDS)}
+    # c09
+    wins = 0
+    for s in SEEDS:
+        hp_p, lp_p = _rates(res, idx[("predictive", s)])
+        margin = min(_rates(res, idx[(b, s)])[0] - hp_p for b in ("temporal", "static", "reactive"))
+        best_lp = min(_rates(res, idx[(b, s)])[1] for b in ("temporal", "static", "reactive"))
+        wins += margin >= 1.0 and lp_p <= best_lp + 5.0
+    assert wins >= 4, f"c09: predictive won only {wins}/5 seeds"
+    # c10
+    full_hp = _rates(res, idx[("predictive", 0)])[0]
+    abl_hp = _rates(res, batch.R - 1)[0]
+    assert full_hp > 0 and abl_hp >= 2.0 * full_hp, f"c10: {full_hp} -> {abl_hp}"
+    # c12: a second launch on the same inputs is identical
+    res2 = batch.run()
+    for k in ("req_status", "req_violated", "req_completion", "dec_gpu", "dec_est_latency", "counters"):
+        assert np.array_equal(res.a[k], res2.a[k], equal_nan=True), k
+    # c13: consumed isolated work equals each batch's isolated kernel latency
+    tab = batch.tab
+    nb = 0
+    for r in range(batch.R):
+        sl = res.replay_slice(r)
+        kern = tab["kernel"][sl["dec_model"].astype(np.int64) * tab["B"] + sl["dec_size"].astype(np.int64) - 1]
+        np.testing.assert_allclose(sl["b_work"], kern, rtol=1e-9)
+        nb += len(kern)
+    assert nb > 10_000
+    # every replay equals the oracle's
+    ores = oracle.replay(batch, threads=4)
+    for r in range(batch.R):
+        d, o = res.replay_slice(r), ores.replay_slice(r)
+        for k in ("req_status", "req_violated", "req_batch", "dec_pass", "dec_gpu", "dec_size", "dec_est_latency"):
+            np.testing.assert_array_equal(d[k], o[k], err_msg=f"replay {r}: {k}")
+        np.testing.assert_array_equal(d["counters"][6:13], o["counters"][6:13])
