@@ -26,6 +26,8 @@ def dev(array, dtype=torch.float64) -> torch.Tensor:
     if isinstance(array, torch.Tensor):
         return array.to(device=device, dtype=dtype).contiguous()
     a = np.ascontiguousarray(array)
+    if not a.flags.writeable:  # torch.from_numpy needs a writable buffer
+        a = a.copy()
     return torch.from_numpy(a).to(device=device, dtype=dtype).contiguous()
 
 

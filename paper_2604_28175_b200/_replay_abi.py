@@ -48,8 +48,23 @@ class ReplayArgs(C.Structure):
                 ("models", ReplayModels)] + [(k, _vp) for k in ARG_ARRAYS]
 
 
+MS_N = 5
+METRIC_ARRAYS = ["window_ms", "req_off", "arr_time", "arr_model", "model_prio", "req_status", "req_violated",
+                 "req_completion", "counters", "dec_model", "dec_size", "dec_est_latency", "b_front",
+                 "b_kernel_start", "b_kernel_end", "b_completion", "fb_predicted", "fb_actual", "kernel_table"]
+METRIC_OUTPUTS = ["class_counts", "partial", "pct", "series_count", "goodput", "goodput_len", "intf_error",
+                  "latency_error", "kernel_overhead"]
+
+
+class MetricsArgs(C.Structure):
+    _fields_ = ([("n_replays", C.c_int32), ("max_windows", C.c_int32)] + [(k, _vp) for k in METRIC_ARRAYS]
+                + [("table_stride", C.c_int32), ("pad", C.c_int32)] + [(k, _vp) for k in METRIC_OUTPUTS])
+
+
 def declare_replay(lib):
     lib.strait_replay.restype = C.c_int
     lib.strait_replay.argtypes = [C.POINTER(ReplayArgs), _vp]
+    lib.strait_replay_metrics.restype = C.c_int
+    lib.strait_replay_metrics.argtypes = [C.POINTER(MetricsArgs), _vp]
     lib.strait_replay_smem_bytes.restype = C.c_int64
     lib.strait_replay_smem_bytes.argtypes = [C.c_int32] * 4

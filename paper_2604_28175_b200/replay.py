@@ -18,7 +18,8 @@ import numpy as np
 import torch
 
 from . import _device as D
-from ._replay_abi import ARG_ARRAYS, POLICY_CODES, RC, RC_N, ReplayArgs, ReplayConfig, ReplayModels
+from ._replay_abi import (ARG_ARRAYS, METRIC_OUTPUTS, MS_N, POLICY_CODES, RC, RC_N, MetricsArgs, ReplayArgs,
+                          ReplayConfig, ReplayModels)
 from .config import ExperimentConfig
 from .domain import PriorityLevel
 from .predictor import InterferencePredictor, PredictorParams, bias_correction_tables
@@ -230,13 +231,50 @@ class ReplayBatch:
                 out[k] = D.dev(v, getattr(torch, np.asarray(v).dtype.name))
         return out
 
-    def run(self, stream=None) -> "ReplayResult":
-        """Host in, one device launch, host out."""
+    # ------------------------------------------------------------------ metrics
+    def max_windows(self) -> int:
+        """Goodput bins that can be non-empty: on-time completions finish by
+        their deadline, i.e. before duration + the largest deadline_ms."""
+        dl = float(np.max(self.tab["deadline"]))
+        return max(int((s.config.workload.duration_ms + dl) // s.config.goodput_window_ms) + 2 for s in self.specs)
+
+    def metrics_args(self, din: dict, dout: dict, mout: dict, ptr) -> MetricsArgs:
+        m = MetricsArgs()
+        m.n_replays, m.max_windows, m.table_stride = self.R, self.max_windows(), self.tab["B"]
+        src = {"window_ms": din["window_ms"], "model_prio": din["tab_prio"], "kernel_table": din["tab_kernel"]}
+        for k in ("req_off", "arr_time", "arr_model"):
+            src[k] = din[k]
+        for k in ("req_status", "req_violated", "req_completion", "counters", "dec_model", "dec_size",
+                  "dec_est_latency", "b_front", "b_kernel_start", "b_kernel_end", "b_completion", "fb_predicted",
+                  "fb_actual"):
+            src[k] = dout[k]
+        for k, v in list(src.items()) + list(mout.items()):
+            setattr(m, k, ptr(v))
+        return m
+
+    def alloc_metrics(self) -> dict:
+        W = self.max_windows()
+        sizes = {"class_counts": (self.R * 8, torch.int64), "partial": (self.R, torch.uint8),
+                 "pct": (self.R * MS_N * 3, torch.float64), "series_count": (self.R * MS_N, torch.int64),
+                 "goodput": (self.R * 2 * W, torch.int64), "goodput_len": (self.R * 2, torch.int32),
+                 "intf_error": (max(self.N, 1), torch.float64), "latency_error": (max(self.N, 1), torch.float64),
+                 "kernel_overhead": (max(self.N, 1), torch.float64)}
+        return {k: D.empty(n, dt) for k, (n, dt) in sizes.items()}
+
+    def run(self, stream=None, metrics: bool = True) -> "ReplayResult":
+        """Host in, device replay (+ device metrics), host out."""
         din = self.device_inputs()
         dout = self.alloc_outputs(device=True)
         args = self.args(din, dout, D.ptr)
         D.check(D.lib().strait_replay(C.byref(args), D.stream_handle(stream)))
-        res = {k: D.host(v) for k, v in dout.items()}
+        res = {}
+        if metrics:
+            din["window_ms"] = D.dev(np.array([s.config.goodput_window_ms for s in self.specs], dtype=np.float64))
+            mout = self.alloc_metrics()
+            margs = self.metrics_args(din, dout, mout, D.ptr)
+            D.check(D.lib().strait_replay_metrics(C.byref(margs), D.stream_handle(stream)))
+            res.update({"m_" + k: D.host(v) for k, v in mout.items()})
+        res.update({k: D.host(v) for k, v in dout.items()})
         res["pred_state"] = D.host(din["pred_state"])
         res["pred_step"] = D.host(din["pred_step"])
         return ReplayResult(self, res)
@@ -255,6 +293,35 @@ class ReplayResult:
 
         for r in range(self.batch.R):
             check_code(int(self.counters[r, RC["ERROR"]]), f"replay {r}")
+
+    def metrics(self, r: int) -> dict:
+        """The replay's metrics in the reference's MetricsReport.to_dict() schema
+        (metrics.py:63-85), from the device metrics kernels."""
+        if "m_pct" not in self.a:
+            raise ValueError("replay ran without metrics")
+        b = self.batch
+        W = b.max_windows()
+        cc = self.a["m_class_counts"].reshape(b.R, 2, 4)[r]
+        pct = self.a["m_pct"].reshape(b.R, MS_N, 3)[r]
+        cnt = self.a["m_series_count"].reshape(b.R, MS_N)[r]
+        gp = self.a["m_goodput"].reshape(b.R, 2, W)[r]
+        glen = self.a["m_goodput_len"].reshape(b.R, 2)[r]
+
+        def opt(x):
+            return None if np.isnan(x) else float(x)
+
+        out = {"window_ms": float(b.specs[r].config.goodput_window_ms), "partial": bool(self.a["m_partial"][r] & 1)}
+        for c, name in ((0, "high"), (1, "low")):
+            arr, comp, drop, viol = (int(x) for x in cc[c])
+            out[name] = {"arrivals": arr, "completed": comp, "dropped": drop, "violations": viol,
+                         "violation_rate_pct": 100.0 * viol / arr if arr else 0.0,
+                         "p50_latency_ms": opt(pct[c][0]), "p95_latency_ms": opt(pct[c][1]),
+                         "p99_latency_ms": opt(pct[c][2]), "goodput_counts": [int(x) for x in gp[c][:glen[c]]]}
+        for s_, name in ((2, "intf_error"), (3, "latency_error"), (4, "kernel_overhead")):
+            n = int(cnt[s_])
+            out[name] = {"count": n, "median_abs": opt(pct[s_][0]), "p95_abs": opt(pct[s_][1]),
+                         "p99_abs": opt(pct[s_][2])} if n else {"count": 0}
+        return out
 
     def violation_rates(self, r: int) -> tuple[float, float]:
         c = self.counters[r]

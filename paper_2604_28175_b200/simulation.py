@@ -23,28 +23,73 @@ import numpy as np
 from .config import ExperimentConfig
 from .domain import PriorityLevel
 from .predictor import InterferencePredictor
-from .replay import ReplayBatch, ReplayResult, ReplaySpec, RC
+from .replay import ReplayBatch, ReplayResult, ReplaySpec
 
 EV_KERNEL_COMPLETE, EV_TRANSFER_COMPLETE, EV_ARRIVAL, EV_BATCH_TIMEOUT, EV_AIMD_TICK = range(5)
 
 
 @dataclass
 class ClassMetrics:
-    arrivals: int
-    dropped: int
-    violations: int
+    """metrics.py:25-50."""
 
-    @property
-    def violation_rate_pct(self) -> float:
-        return 100.0 * self.violations / self.arrivals if self.arrivals else 0.0
+    arrivals: int = 0
+    completed: int = 0
+    dropped: int = 0
+    violations: int = 0
+    violation_rate_pct: float = 0.0
+    p50_latency: Optional[float] = None
+    p95_latency: Optional[float] = None
+    p99_latency: Optional[float] = None
+    goodput_counts: list = field(default_factory=list)
+
+    def to_dict(self) -> dict:
+        return {"arrivals": self.arrivals, "completed": self.completed, "dropped": self.dropped,
+                "violations": self.violations, "violation_rate_pct": self.violation_rate_pct,
+                "p50_latency_ms": self.p50_latency, "p95_latency_ms": self.p95_latency,
+                "p99_latency_ms": self.p99_latency, "goodput_counts": list(self.goodput_counts)}
 
 
 @dataclass
 class MetricsReport:
-    """The per-class counts of metrics.compute_metrics (metrics.py:88-158) that
-    the parity contract covers; percentiles/goodput are host post-processing."""
+    """metrics.py:53-85, computed on the device (strait_replay_metrics)."""
 
-    per_class: dict = field(default_factory=dict)
+    per_class: dict
+    window_ms: float
+    intf_error: list
+    latency_error: list
+    kernel_overhead: list
+    cap_timeline: list
+    partial: bool = False
+    _stats: dict = field(default_factory=dict, repr=False)
+
+    def goodput_per_s(self, priority: PriorityLevel) -> list[float]:
+        scale = 1000.0 / self.window_ms
+        return [c * scale for c in self.per_class[priority].goodput_counts]
+
+    def to_dict(self) -> dict:
+        d = {"window_ms": self.window_ms, "partial": self.partial,
+             "high": self.per_class[PriorityLevel.HIGH].to_dict(), "low": self.per_class[PriorityLevel.LOW].to_dict()}
+        d.update(self._stats)
+        return d
+
+
+def _report(res: ReplayResult, r: int) -> MetricsReport:
+    d = res.metrics(r)
+    per = {}
+    for p, name in ((PriorityLevel.HIGH, "high"), (PriorityLevel.LOW, "low")):
+        c = d[name]
+        per[p] = ClassMetrics(c["arrivals"], c["completed"], c["dropped"], c["violations"], c["violation_rate_pct"],
+                              c["p50_latency_ms"], c["p95_latency_ms"], c["p99_latency_ms"], c["goodput_counts"])
+    sl = res.replay_slice(r)
+    lo = int(res.batch.inputs["req_off"][r])
+    nb = len(sl["dec_time"])
+    order = np.argsort(sl["b_done_order"], kind="stable")  # feedback / batch rows are in completion order
+    series = {k: res.a["m_" + k][lo:lo + nb][order].tolist() for k in ("intf_error", "latency_error",
+                                                                       "kernel_overhead")}
+    caps = [(float(t), int(g), float(c)) for t, g, c in zip(sl["cap_time"], sl["cap_gpu"], sl["cap_pct"])]
+    return MetricsReport(per, d["window_ms"], series["intf_error"], series["latency_error"],
+                         series["kernel_overhead"], caps, d["partial"],
+                         {k: d[k] for k in ("intf_error", "latency_error", "kernel_overhead")})
 
 
 @dataclass
@@ -154,13 +199,6 @@ class Simulation:
         return run_many([ReplaySpec(self.cfg, self.seed, self.predictor)])[0]
 
 
-def _metrics(c) -> MetricsReport:
-    return MetricsReport({
-        "high": ClassMetrics(int(c[RC["HP_ARR"]]), int(c[RC["HP_DROP"]]), int(c[RC["HP_VIOL"]])),
-        "low": ClassMetrics(int(c[RC["LP_ARR"]]), int(c[RC["LP_DROP"]]), int(c[RC["LP_VIOL"]])),
-    })
-
-
 def run_many(specs: list[ReplaySpec]) -> list[SimResult]:
     """Many independent replays in ONE device launch (the analogue of
     `infersim sweep`, cli.py:64-103).  Injected predictors are refit in place."""
@@ -178,7 +216,7 @@ def run_many(specs: list[ReplaySpec]) -> list[SimResult]:
             s.predictor.opt.v = list(st[2 * np_:])
             s.predictor.opt.step = int(sl["pred_step"])
         seed = s.config.seed if s.seed is None else s.seed
-        out.append(SimResult(s.config.policy, s.config.policy_variant, seed, res, r, _metrics(sl["counters"])))
+        out.append(SimResult(s.config.policy, s.config.policy_variant, seed, res, r, _report(res, r)))
     return out
 
 

@@ -420,6 +420,10 @@ def reference_replay_arrays(name, tmpdir):
     m = res.metrics.per_class
     out["class_counts"] = np.array([[m[c].arrivals, m[c].dropped, m[c].violations] for c in PriorityLevel])
     out["trace_hash"] = np.array(res.trace_hash())
+    # the reference's own metrics (metrics.py:88-158), window = config.goodput_window_ms
+    import json
+    out["metrics_json"] = np.array(json.dumps(res.metrics.to_dict()))
+    out["goodput_window_ms"] = np.array(rcfg.goodput_window_ms)
     return out
 
 

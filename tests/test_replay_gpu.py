@@ -145,3 +145,20 @@ def test_replay_rejects_unsupported_geometry(cuda):
 
     with pytest.raises(ValueError):
         device_run([ReplaySpec(MC.config_from_dict(overload_doc(100, concurrency_limit=9)))])
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_replay_metrics_vs_reference(cuda, name):
+    """Device compute_metrics (strait_replay_metrics) equals the reference's
+    MetricsReport.to_dict() of the same replay — counts, exact nearest-rank
+    percentiles, goodput windows and the error-series statistics."""
+    import json
+
+    from paper_2604_28175_b200.replay import ReplaySpec
+
+    g = load(name)
+    _, res = device_run([ReplaySpec(case_config(name))])
+    got = res.metrics(0)
+    want = json.loads(str(g["metrics_json"]))
+    want.pop("window_ms"), got.pop("window_ms")
+    assert got == want

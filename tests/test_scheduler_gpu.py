@@ -285,8 +285,13 @@ def test_run_drop_in_matches_reference_golden(cuda):
     np.testing.assert_array_equal([r["batch"] for r in fb], [f"b{b}" for b in done])
     req = res.request_rows
     assert sum(r["violated"] for r in req) == int(g["class_counts"][:, 2].sum())
-    hp = res.metrics.per_class["high"]
+    from paper_2604_28175_b200.domain import PriorityLevel
+
+    hp = res.metrics.per_class[PriorityLevel.HIGH]
     assert (hp.arrivals, hp.dropped, hp.violations) == tuple(int(x) for x in g["class_counts"][0])
+    import json
+
+    assert res.metrics.to_dict() == json.loads(str(g["metrics_json"]))  # metrics.py MetricsReport, on device
     assert len(res.cap_rows) == len(g["cap_time"])
 
 
