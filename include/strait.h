@@ -65,10 +65,10 @@ void strait_host_exp(const double *x, double *y, int64_t n);
 
 /*
  * Elementwise device math with the reference host's bits: fn 0 exp(x),
- * 1 log(x), 2 pow(x, y) — restatements of glibc 2.39's exp/log/pow (the
- * libm behind CPython's math.exp, math.log and float.__pow__, which
- * predictor.py:136-137,181-184,289-293 and oracle.py:73 call).  y may be NULL
- * unless fn == 2.
+ * 1 log(x), 2 pow(x, y), 3 log1p(x) — restatements of glibc 2.39's
+ * exp/log/pow/log1p (the libm behind CPython's math.exp, math.log and
+ * float.__pow__, which predictor.py:136-137,181-184,289-293 and oracle.py:73
+ * call, and behind numpy's ziggurat tails).  y may be NULL unless fn == 2.
  */
 int strait_math(int32_t fn, const double *x, const double *y, int64_t n, double *out, void *stream);
 

@@ -156,6 +156,10 @@ def _declare(lib):
         from ._replay_abi import declare_replay
 
         declare_replay(lib)
+    if hasattr(lib, "strait_stream_count"):
+        from .devgen import declare
+
+        declare(lib)
 
 
 def lib():

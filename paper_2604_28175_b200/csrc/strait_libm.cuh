@@ -250,5 +250,84 @@ __device__ __forceinline__ double pow(double x, double y) {
   return exp_core<true>(ehi, elo, sign_bias, abstop, exp_table());
 }
 
+// math.log1p / numpy's npy_log1p (s_log1p.c, fdlibm algorithm; glibc's FMA
+// build __log1p_fma).  Used by numpy's ziggurat tails (distributions.c).
+__device__ __forceinline__ double set_high(double u, uint32_t hi) {
+  return as_d(((uint64_t)hi << 32) | (as_u(u) & 0xffffffffull));
+}
+__device__ __forceinline__ double log1p(double x) {
+  constexpr double ln2_hi = 0x1.62e42fee00000p-1, ln2_lo = 0x1.a39ef35793c76p-33;
+  constexpr double Lp1 = 0x1.5555555555593p-1, Lp2 = 0x1.999999997fa04p-2, Lp3 = 0x1.2492494229359p-2;
+  constexpr double Lp4 = 0x1.c71c51d8e78afp-3, Lp5 = 0x1.7466496cb03dep-3, Lp6 = 0x1.39a09d078c69fp-3;
+  constexpr double Lp7 = 0x1.2f112df3e5244p-3;
+  const int32_t hx = (int32_t)(as_u(x) >> 32);
+  const uint32_t ax = (uint32_t)hx & 0x7fffffffu;
+  int k = 1, hu = 0;
+  double f = 0.0, c = 0.0;
+  if (hx < 0x3FDA827A) {                           // x < 0.41422
+    if (ax >= 0x3ff00000u) {                       // x <= -1
+      if (x == -1.0) return __longlong_as_double(0xfff0000000000000LL);
+      return __longlong_as_double(0x7ff8000000000000LL);
+    }
+    if (ax < 0x3e200000u) {                        // |x| < 2^-29
+      if (ax < 0x3c900000u) return x;              // |x| < 2^-54
+      return __fma_rn(-(x * x), 0.5, x);           // fma: x - x*x*0.5
+    }
+    if ((uint32_t)hx + 0x402d413cu > 0x402d413cu) {  // -0.2929 < x < 0.41422
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  } else if (hx > 0x7fefffff) {
+    return x + x;
+  }
+  if (k != 0) {
+    double u;
+    if (hx < 0x43400000) {
+      u = 1.0 + x;
+      hu = (int)(as_u(u) >> 32);
+      k = (hu >> 20) - 1023;
+      c = (k > 0) ? 1.0 - (u - x) : x - (u - 1.0);  // correction term
+      c = __ddiv_rn(c, u);
+    } else {
+      u = x;
+      hu = (int)(as_u(u) >> 32);
+      k = (hu >> 20) - 1023;
+      c = 0.0;
+    }
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = set_high(u, (uint32_t)hu | 0x3ff00000u);  // normalize u
+    } else {
+      k += 1;
+      u = set_high(u, (uint32_t)hu | 0x3fe00000u);  // normalize u/2
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = u - 1.0;
+  }
+  const double hfsq = (f * 0.5) * f;
+  const double kd = (double)k;
+  if (hu == 0) {  // |f| < 2^-20
+    if (f == 0.0) {
+      if (k == 0) return 0.0;
+      return __fma_rn(kd, ln2_hi, __fma_rn(kd, ln2_lo, c));  // fma x2: c += k*ln2_lo; k*ln2_hi + c
+    }
+    const double R = __fma_rn(-f, 0x1.5555555555555p-1, 1.0) * hfsq;  // fma: hfsq*(1.0 - 0.666..*f)
+    if (k == 0) return f - R;
+    return __fma_rn(kd, ln2_hi, -((R - __fma_rn(kd, ln2_lo, c)) - f));
+  }
+  const double s = __ddiv_rn(f, f + 2.0);
+  const double z = s * s;
+  const double R2 = __fma_rn(z, Lp3, Lp2), R3 = __fma_rn(z, Lp5, Lp4), R4 = __fma_rn(z, Lp7, Lp6);
+  const double z2 = z * z, z4 = z2 * z2, z6 = z2 * z4;
+  double R = __fma_rn(z, Lp1, z2 * R2);  // fma: R1 + z2*R2, R1 = z*Lp1
+  R = __fma_rn(z4, R3, R);
+  R = __fma_rn(z6, R4, R);
+  const double q = (R + hfsq) * s;  // s*(hfsq+R)
+  if (k == 0) return f - (hfsq - q);
+  const double w = __fma_rn(kd, ln2_lo, c) + q;
+  return __fma_rn(kd, ln2_hi, -((hfsq - w) - f));  // fmsub: k*ln2_hi - ((hfsq - (...)) - f)
+}
+
 }  // namespace glibc
 }  // namespace strait

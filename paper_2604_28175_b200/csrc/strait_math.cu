@@ -12,13 +12,14 @@ __global__ void math_kernel(int fn, const double* __restrict__ x, const double* 
                             double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double a = x[i];
-    out[i] = fn == 0 ? strait::dexp(a) : fn == 1 ? strait::dlog(a) : strait::dpow(a, y[i]);
+    out[i] = fn == 0 ? strait::dexp(a) : fn == 1 ? strait::dlog(a) : fn == 2 ? strait::dpow(a, y[i])
+                                                                  : strait::glibc::log1p(a);
   }
 }
 }  // namespace
 
 extern "C" int strait_math(int32_t fn, const double* x, const double* y, int64_t n, double* out, void* stream) {
-  if (fn < 0 || fn > 2 || n < 0 || (n && (!x || !out || (fn == 2 && !y))))
+  if (fn < 0 || fn > 3 || n < 0 || (n && (!x || !out || (fn == 2 && !y))))
     return strait::set_error(STRAIT_EINVAL, "strait_math: bad arguments");
   if (!n) return STRAIT_OK;
   const int64_t blocks64 = (n + 255) / 256;

@@ -122,9 +122,15 @@ def replay_config(cfg: ExperimentConfig, pred: InterferencePredictor) -> ReplayC
 class ReplayBatch:
     """Host inputs of a batch of replays sharing one profile set."""
 
-    def __init__(self, specs: Sequence[ReplaySpec], cap_rows_max: Optional[int] = None):
+    def __init__(self, specs: Sequence[ReplaySpec], cap_rows_max: Optional[int] = None, generate: str = "host"):
+        """generate="host": draw the arrival / noise streams with numpy here;
+        generate="device": draw the same streams on the GPU (devgen.py)."""
         if not specs:
             raise ValueError("empty replay batch")
+        if generate not in ("host", "device"):
+            raise ValueError(f"generate must be 'host' or 'device', got {generate!r}")
+        self.generate = generate
+        self._dev = {}
         self.specs = list(specs)
         prof = self.specs[0].config.profiles
         for s in self.specs:
@@ -140,6 +146,11 @@ class ReplayBatch:
             seed = cfg.seed if s.seed is None else s.seed
             pred = s.predictor or InterferencePredictor(PredictorParams(weights=(0.1,) * nm))
             self.preds.append(pred)
+            cfgs.append(replay_config(cfg, pred))
+            states.append(pred.params.to_vector() + list(pred.opt.m) + list(pred.opt.v))
+            steps.append(pred.opt.step)
+            if generate == "device":
+                continue
             streams = cfg.workload.generate_arrays(seed)
             per = [np.asarray(streams.get(mid, np.empty(0)), dtype=np.float64) for mid in self.tab["ids"]]
             counts = np.array([len(x) for x in per], dtype=np.int64)
@@ -161,9 +172,14 @@ class ReplayBatch:
             else:
                 noise.append(np.ones(n))
             req_off.append(base + n)
-            cfgs.append(replay_config(cfg, pred))
-            states.append(pred.params.to_vector() + list(pred.opt.m) + list(pred.opt.v))
-            steps.append(pred.opt.step)
+        if generate == "device":
+            from . import devgen
+
+            items = [(s.config.workload, s.config.seed if s.seed is None else s.seed, s.config.ground_truth.noise_sigma)
+                     for s in self.specs]
+            g = devgen.generate(items, self.tab["ids"])
+            self._dev = {k: g[k] for k in ("arr_time", "arr_model", "model_req", "noise")}
+            req_off, mr_off = g["req_off"].tolist(), g["mr_off"].tolist()
         betas = {(p.opt.beta1, p.opt.beta2) for p in self.preds}
         if len(betas) != 1:
             raise ValueError("all replays of a batch must share the Adam betas")
@@ -178,14 +194,15 @@ class ReplayBatch:
                 for s in self.specs)
         self.cap_rows_max = int(cap_rows_max)
         self.inputs = {
-            "req_off": np.asarray(req_off, dtype=np.int64),
-            "arr_time": np.concatenate(arr_t), "arr_model": np.concatenate(arr_m),
-            "model_req": np.concatenate(model_req), "mr_off": np.asarray(mr_off, dtype=np.int64),
-            "noise": np.concatenate(noise), "bc1": bc1, "bc2": bc2,
+            "req_off": np.asarray(req_off, dtype=np.int64), "mr_off": np.asarray(mr_off, dtype=np.int64),
+            "bc1": bc1, "bc2": bc2,
             "pred_state": np.asarray(states, dtype=np.float64).ravel(),
             "pred_step": np.asarray(steps, dtype=np.int64),
             "cfg": (ReplayConfig * self.R)(*cfgs),
         }
+        if generate == "host":
+            self.inputs.update(arr_time=np.concatenate(arr_t), arr_model=np.concatenate(arr_m),
+                               model_req=np.concatenate(model_req), noise=np.concatenate(noise))
 
     # ------------------------------------------------------------------ buffers
     def alloc_outputs(self, device: bool):
@@ -216,14 +233,18 @@ class ReplayBatch:
 
     def host_inputs(self) -> dict:
         d = dict(self.inputs)
+        for k, v in self._dev.items():  # device-generated streams (copied back for host checkers)
+            d[k] = D.host(v)[:max(self.N, 1)]
         for k in ("max_batch", "prio", "deadline", "timeout", "total", "transfer", "kernel", "self_cmp",
                   "self_mem", "throughput"):
             d["tab_" + k] = np.ascontiguousarray(self.tab[k])
         return d
 
     def device_inputs(self) -> dict:
-        out = {}
+        out = dict(self._dev)
         for k, v in self.host_inputs().items():
+            if k in out:
+                continue
             if k == "cfg":
                 buf = np.frombuffer(bytes(v), dtype=np.uint8)
                 out[k] = D.dev(buf, torch.uint8)

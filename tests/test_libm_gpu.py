@@ -73,3 +73,13 @@ def test_pow_bit_exact(cuda):
     special_b = np.array([2.0, 2.0, 1.0, math.e, math.e, math.e, 0.5, 10.0, 10.0])
     special_e = np.array([0.0, -0.0, 123.0, 1e-30, -1e-30, 1e20, 1074.5, 400.0, -400.0])
     _check(2, lambda a, b: a ** b, np.concatenate([base, special_b]), np.concatenate([expo, special_e]))
+
+
+def test_log1p_bit_exact(cuda):
+    """numpy's ziggurat tails call log1p(-u), u in [0, 1) (distributions.c)."""
+    rng = np.random.default_rng(10)
+    u = (rng.integers(0, 2 ** 53, 300_000, dtype=np.int64) * 2.0 ** -53)
+    x = np.concatenate([-u, rng.uniform(-0.999, 5.0, 100_000), rng.normal(0, 1e-6, 20_000),
+                        np.exp(rng.uniform(-40, 40, 20_000)), [0.0, -0.0, -0.5, -0.2929, 0.41422, 1e-300,
+                                                                -1e-20, 3e-9, 2.0 ** 53, 1e300]])
+    _check(3, math.log1p, x)
