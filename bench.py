@@ -182,9 +182,9 @@ def replay_cpu(specs, seconds: float, threads: int):
 
 
 def replay_leg(args, ws, rank, local, dist):
-    """Device time of the whole C4 sweep (inputs resident) + the same through
-    the public API with host buffers (pinned H2D of every input, D2H of the
-    per-request outcomes and counters)."""
+    """Device time of the whole C4 sweep (inputs resident in HBM) + the same
+    through the public API end to end (ReplayBatch(specs, generate="device")
+    .run(): host configs in, per-request outcomes + counters + metrics out)."""
     import ctypes as Cc
 
     import torch
@@ -194,10 +194,10 @@ def replay_leg(args, ws, rank, local, dist):
 
     specs, n_total = c4_shard(args, ws, rank)
     t0 = time.perf_counter()
-    batch = ReplayBatch(specs)
+    batch = ReplayBatch(specs, generate="device")  # streams drawn on the GPU
+    torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     lib = D.lib()
-    host_in = batch.host_inputs()
     din = batch.device_inputs()
     dout = batch.alloc_outputs(device=True)
     cargs = batch.args(din, dout, D.ptr)
@@ -225,30 +225,27 @@ def replay_leg(args, ws, rank, local, dist):
     launches = (lib.strait_kernel_launches() - l0) / args.replay_steps
     counters = D.host(dout["counters"]).reshape(batch.R, -1)
     assert (counters[:, RC["ERROR"]] == 0).all(), "replay error"
-    # end to end through the C-ABI with host buffers
-    keys = [k for k in host_in if k != "cfg"]
-    pinned = {k: torch.from_numpy(np.ascontiguousarray(host_in[k])).pin_memory() for k in keys}
-    pinned["cfg"] = torch.frombuffer(bytearray(bytes(host_in["cfg"])), dtype=torch.uint8).pin_memory()
-    h2d = sum(t.numel() * t.element_size() for t in pinned.values())
-    outs = ("counters", "req_status", "req_violated")
-    hout = {k: torch.empty(dout[k].shape, dtype=dout[k].dtype, pin_memory=True) for k in outs}
-    d2h = sum(t.numel() * t.element_size() for t in hout.values())
+    # end to end through the public API: ReplayBatch(specs, generate="device").run() — the
+    # stream descriptions and configs go host->device, the arrival / noise streams are drawn
+    # on the GPU (draw-for-draw numpy's), the replays and compute_metrics run there, and the
+    # per-request outcomes + counters + metrics come back.
+    fetch = {"counters", "req_status", "req_violated"}
     e2e = []
-    for i in range(2):
+    del din, dout, cargs  # the resident-input buffers above are not part of the API call
+    for i in range(3):
+        b2 = res2 = None  # release the previous call's outputs before the next one allocates
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for k, t in pinned.items():
-            din[k].copy_(t, non_blocking=True)
-        D.check(lib.strait_replay(Cc.byref(cargs), stream.cuda_stream))
-        for k in outs:
-            hout[k].copy_(dout[k], non_blocking=True)
-        e1.record()
+        t0 = time.perf_counter()
+        b2 = ReplayBatch(specs, generate="device")
+        res2 = b2.run(metrics=True, fetch=fetch)
         torch.cuda.synchronize()
         if i:
-            e2e.append(e0.elapsed_time(e1))
+            e2e.append((time.perf_counter() - t0) * 1e3)
+    h2d = int(sum(np.asarray(v).nbytes for k, v in b2.inputs.items() if k != "cfg") + len(bytes(b2.inputs["cfg"])))
+    d2h = int(sum(v.nbytes for k, v in res2.a.items() if k in fetch or k.startswith("m_")))
+    hout = {"counters": torch.from_numpy(res2.a["counters"])}
     c = hout["counters"].numpy().reshape(batch.R, -1)
-    vec = torch.tensor([dev_ms, e2e[0], build_s, 0, 0, 0, 0, 0, 0], dtype=torch.float64, device="cuda")
+    vec = torch.tensor([dev_ms, float(np.mean(e2e)), build_s, 0, 0, 0, 0, 0, 0], dtype=torch.float64, device="cuda")
     vec[3:] = torch.tensor([batch.N, c[:, RC["HP_ARR"]].sum(), c[:, RC["LP_ARR"]].sum(), c[:, RC["HP_VIOL"]].sum(),
                             c[:, RC["LP_VIOL"]].sum(), c[:, RC["BATCHES"]].sum()], dtype=torch.float64)
     if ws > 1:  # the only collective: max of the times, sum of the counters (NCCL)
@@ -264,7 +261,8 @@ def replay_leg(args, ws, rank, local, dist):
            "hp_violation_pct": 100.0 * hp_v / max(hp_arr, 1), "lp_violation_pct": 100.0 * lp_v / max(lp_arr, 1),
            "e2e": {"value": n_req / (e2e_ms / 1e3), "unit": REPLAY_UNIT, "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                   "path": "pinned host inputs -> H2D -> strait_replay (C-ABI) -> D2H outcomes"},
+                   "path": "ReplayBatch(specs, generate='device').run(): configs + stream specs H2D -> "
+                           "device streams -> strait_replay -> device metrics -> D2H outcomes (wall clock)"},
            "host_input_build_s": build_s, "gpu_launches": launches,
            "bound": "latency (one warp per replay); no roofline claim, DESIGN.md 3.3"}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -41,16 +41,15 @@ constexpr int kMaxP = STRAIT_MAX_METRICS + 7;
 __host__ __device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
 __host__ __device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
 
-// exp of the predictor's effect (a kernel may route it to a shared, non-inlined copy)
-#ifndef STRAIT_PRED_EXP
-#define STRAIT_PRED_EXP(z, tab) dexp(z, tab)
-#endif
-#ifndef STRAIT_PRED_LOG
-#define STRAIT_PRED_LOG(x) dlog(x)
-#endif
+// Transcendental policy of the predictor: inlined (default), or routed by a
+// kernel to shared out-of-line copies (MathT with the same static members).
+struct InlineMath {
+  static __device__ __forceinline__ double exp(double x, const ulonglong2* tab) { return dexp(x, tab); }
+  static __device__ __forceinline__ double log(double x) { return dlog(x); }
+};
 
 // Parameters of one predictor, staged in registers/shared memory by callers.
-template <int NM>
+template <int NM, typename MathT = InlineMath>
 struct Pred {
   double scale, offset, log_base;  // log_base = math.log(params.base), hoisted (same value per call)
   double w[NM];
@@ -61,7 +60,7 @@ struct Pred {
 
   __device__ __forceinline__ void load(const double* __restrict__ P, double effect_cap) {
     scale = P[0];
-    log_base = STRAIT_PRED_LOG(P[1]);
+    log_base = MathT::log(P[1]);
     offset = P[2];
 #pragma unroll
     for (int i = 0; i < NM; ++i) w[i] = P[3 + i];
@@ -90,7 +89,7 @@ struct Pred {
       saturated = true;
       return cap;
     }
-    const double inner = scale * STRAIT_PRED_EXP(z, etab) + offset;
+    const double inner = scale * MathT::exp(z, etab) + offset;
     saturated = inner >= cap;
     if (saturated) return cap;
     return py_min(py_max(inner, 0.0), cap);

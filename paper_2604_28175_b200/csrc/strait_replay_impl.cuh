@@ -36,31 +36,37 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "../../include/strait_replay.h"
 #include "strait_capi.cuh"
 
-// The engine's hot loop is large and every warp sits at a different point of
-// it, so instruction-cache footprint matters more than call overhead: exp,
-// log and pow get ONE out-of-line copy each per translation unit.
-namespace strait {
-namespace rp {
-static __device__ __noinline__ double rp_exp(double x);
-static __device__ __noinline__ double rp_log(double x);
-static __device__ __noinline__ double rp_pow(double x, double y);
-}  // namespace rp
-}  // namespace strait
-#define STRAIT_PRED_EXP(z, tab) ::strait::rp::rp_exp(z)
-#define STRAIT_PRED_LOG(x) ::strait::rp::rp_log(x)
 #include "strait_device.cuh"
 
 namespace strait {
 namespace rp {
 
+// Two math policies.  The latency variant (few replays, one warp each: C2,
+// C4's longest replays bound the launch) inlines everything.  The throughput
+// variant (16 replays per SM) is instruction-cache bound — 16 warps at
+// different points of the hot loop — so exp, log, pow and the IEEE division
+// get ONE out-of-line copy each.  Both return identical bits.
 static __device__ __noinline__ double rp_exp(double x) { return dexp(x); }
 static __device__ __noinline__ double rp_log(double x) { return dlog(x); }
 static __device__ __noinline__ double rp_pow(double x, double y) { return dpow(x, y); }
-// IEEE binary64 division (same result as `a / b`; one out-of-line copy)
 static __device__ __noinline__ double rp_div(double a, double b) { return __ddiv_rn(a, b); }
+
+struct OutlineMath {
+  static __device__ __forceinline__ double exp(double x, const ulonglong2*) { return rp_exp(x); }
+  static __device__ __forceinline__ double log(double x) { return rp_log(x); }
+  static __device__ __forceinline__ double pow(double x, double y) { return rp_pow(x, y); }
+  static __device__ __forceinline__ double div(double a, double b) { return rp_div(a, b); }
+};
+struct FullInlineMath : InlineMath {
+  static __device__ __forceinline__ double exp(double x, const ulonglong2* tab) { return dexp(x, tab); }
+  static __device__ __forceinline__ double pow(double x, double y) { return dpow(x, y); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+};
 
 constexpr int kKC = 0, kTC = 1, kARR = 2, kTO = 3, kTICK = 4;  // simulation.py:28-33 tie ranks
 constexpr double kWorkEps = 1e-9;                               // simulation.py:35
@@ -115,7 +121,7 @@ struct Layout {
   }
 };
 
-template <int NM>
+template <int NM, typename MathT>
 struct Sim {
   static constexpr int NP = NM + 7;
   static constexpr int SD_ACC = SD_VL + NM;   // timeline integral
@@ -136,7 +142,7 @@ struct Sim {
   int *si, *gi, *qi;
   int8_t *sb, *go, *qb;
   // ---- uniform scalar state (identical in every lane)
-  Pred<NM> pr;
+  Pred<NM, MathT> pr;
   double adam_m, adam_v;  // lane-owned Adam moments (lane k owns parameter k)
   int64_t step;
   unsigned long long seq;
@@ -244,7 +250,7 @@ struct Sim {
     }
     const double d = end - SD(SD_TL, s);
 #pragma unroll
-    for (int i = 0; i < NM; ++i) out[i] = rp_div(SD(SD_ACC + i, s) + SD(SD_VL + i, s) * d, total);
+    for (int i = 0; i < NM; ++i) out[i] = MathT::div(SD(SD_ACC + i, s) + SD(SD_VL + i, s) * d, total);
   }
 
   // ------------------------------------------------------------ runtime (runtime.py:104-141)
@@ -288,7 +294,7 @@ struct Sim {
     double x = cf->gt_w_cmp * SD(SD_CMP, s) + cf->gt_w_mem * SD(SD_MEM, s);
 #pragma unroll
     for (int i = 0; i < NM; ++i) x += cf->gt_w[i] * SD(SD_AEX + i, s);
-    double effect = cf->gt_family == 0 ? cf->gt_scale * rp_pow(cf->gt_base, x) + cf->gt_offset
+    double effect = cf->gt_family == 0 ? cf->gt_scale * MathT::pow(cf->gt_base, x) + cf->gt_offset
                                        : cf->gt_scale * x * x + cf->gt_offset;
     effect = py_max(0.0, effect);
     return 1.0 + effect * (SB(SB_PRIO, s) == 0 ? cf->gt_pf_high : cf->gt_pf_low) * SD(SD_NOISE, s);
@@ -300,7 +306,7 @@ struct Sim {
     bool ok = !(d < 0);
     if (d > 0) {
       const double slow = SD(SD_SLOW, s);
-      const double q = rp_div(d, slow);  // the reference divides twice; same value
+      const double q = MathT::div(d, slow);  // the reference divides twice; same value
       SD(SD_WORK, s) = SD(SD_WORK, s) + q;
       double rem = SD(SD_REM, s) - q;
       if (rem < -kWorkEps) ok = false;
@@ -344,7 +350,7 @@ struct Sim {
   __device__ __forceinline__ void reactive_catch_up(double now) {
     const double period = cf->reactive_period;
     if (now - last_reset >= period) {
-      const double periods = floor(rp_div(now - last_reset, period));
+      const double periods = floor(MathT::div(now - last_reset, period));
       lp_allowance = cf->reactive_default;
       last_reset += periods * period;
     }
@@ -393,7 +399,7 @@ struct Sim {
       saturated = true;
       inner = __longlong_as_double(0x7ff0000000000000LL);
     } else {
-      pow_bx = rp_exp(z);
+      pow_bx = MathT::exp(z, pr.etab);
       inner = pr.scale * pow_bx + pr.offset;
       saturated = inner >= cap;
     }
@@ -407,7 +413,7 @@ struct Sim {
       const double log_b = pr.log_base;
       const double zz = pr.scale * pow_bx;
       if (lane == 0) d = pow_bx * cfc;
-      else if (lane == 1) d = pr.scale * x * rp_exp((x - 1.0) * log_b) * cfc;
+      else if (lane == 1) d = pr.scale * x * MathT::exp((x - 1.0) * log_b, pr.etab) * cfc;
       else if (lane == 2) d = cfc;
       else if (lane < 3 + NM) {
         double ai = 0.0;
@@ -434,9 +440,9 @@ struct Sim {
     if (owner && lane != other) {
       adam_m = b1 * adam_m + (1.0 - b1) * gk;
       adam_v = b2 * adam_v + (1.0 - b2) * gk * gk;
-      const double m_hat = rp_div(adam_m, bc1);
-      const double v_hat = rp_div(adam_v, bc2);
-      p -= rp_div(cf->learning_rate * m_hat, sqrt(v_hat) + cf->eps);
+      const double m_hat = MathT::div(adam_m, bc1);
+      const double v_hat = MathT::div(adam_v, bc2);
+      p -= MathT::div(cf->learning_rate * m_hat, sqrt(v_hat) + cf->eps);
       if (lane == 0) p = py_max(p, 1e-6);        // enforce_floors (predictor.py:98-102)
       if (lane == 1) p = py_max(p, 1.0 + 1e-6);
     }
@@ -484,7 +490,7 @@ struct Sim {
   // check_violate (scheduler.py:118-161) of the candidate on GPU g; lane-local.
   __device__ __forceinline__ bool violate(int g, const Cand& cd, int cprio, double now) const {
     if (cprio == 1) {  // LOW: LP aggregate + contribution vs the AIMD cap (:130-135)
-      const double capf = rp_div(GD(GD_CAP, g), 100.0);
+      const double capf = MathT::div(GD(GD_CAP, g), 100.0);
 #pragma unroll
       for (int i = 0; i < NM; ++i)
         if (GD(GD_LPA + i, g) + cd.c[i] > capf) return true;
@@ -502,7 +508,7 @@ struct Sim {
       const double ks = SD(SD_KS, s), tk = SD(SD_TK, s);
       const double elapsed = py_max(0.0, now - ks);
       const double denom = intf_cur * tk;
-      const double progress = denom > 0 ? py_min(1.0, rp_div(elapsed, denom)) : 1.0;
+      const double progress = denom > 0 ? py_min(1.0, MathT::div(elapsed, denom)) : 1.0;
       const double remaining = (1.0 - progress) * tk * intf_new;
       const double projected = py_max(now, ks) + remaining;
       if (projected > SD(SD_DL, s)) return true;
@@ -946,7 +952,7 @@ struct Sim {
     double tw[NM];
     tl_twa(s, now, tw);
     const double tk = tab_kernel(m, k);
-    const double actual = rp_div(measured, tk);
+    const double actual = MathT::div(measured, tk);
     if (!(actual > 0)) fail(STRAIT_EINVAL);
     // GpuRuntimeState.remove_entry (runtime.py:132-141): shift the running list
     const int n = GI(GI_NRUN, g);
@@ -994,7 +1000,7 @@ struct Sim {
       if (g < NG) {
         const double old = GD(GD_CAP, g), last = GD(GD_TICK, g);
         if (now < last) bad = true;
-        const double whole = floor(rp_div(now - last, cf->aimd_interval));
+        const double whole = floor(MathT::div(now - last, cf->aimd_interval));
         cap = old;
         if (whole > 0) {
           cap = py_min(cf->aimd_ceiling, old + whole * cf->aimd_increase);
@@ -1180,7 +1186,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   if (r >= a.n_replays) return;
   const Layout L(a.max_gpus, a.max_concurrency, a.models.n_models, NM);
   unsigned char* base = smem + (size_t)w * L.bytes;
-  Sim<NM> S;
+  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type> S;
   S.A = &a;
   S.cf = a.cfg + r;
   S.lane = threadIdx.x & 31;

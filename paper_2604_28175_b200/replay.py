@@ -231,20 +231,22 @@ class ReplayBatch:
             setattr(a, k, ptr(src[k]))
         return a
 
-    def host_inputs(self) -> dict:
+    def _host_small(self) -> dict:
         d = dict(self.inputs)
-        for k, v in self._dev.items():  # device-generated streams (copied back for host checkers)
-            d[k] = D.host(v)[:max(self.N, 1)]
         for k in ("max_batch", "prio", "deadline", "timeout", "total", "transfer", "kernel", "self_cmp",
                   "self_mem", "throughput"):
             d["tab_" + k] = np.ascontiguousarray(self.tab[k])
         return d
 
+    def host_inputs(self) -> dict:
+        d = self._host_small()
+        for k, v in self._dev.items():  # device-generated streams (copied back for host checkers)
+            d[k] = D.host(v)[:max(self.N, 1)]
+        return d
+
     def device_inputs(self) -> dict:
-        out = dict(self._dev)
-        for k, v in self.host_inputs().items():
-            if k in out:
-                continue
+        out = dict(self._dev)  # device-generated streams stay where they are
+        for k, v in self._host_small().items():
             if k == "cfg":
                 buf = np.frombuffer(bytes(v), dtype=np.uint8)
                 out[k] = D.dev(buf, torch.uint8)
@@ -282,8 +284,9 @@ class ReplayBatch:
                  "kernel_overhead": (max(self.N, 1), torch.float64)}
         return {k: D.empty(n, dt) for k, (n, dt) in sizes.items()}
 
-    def run(self, stream=None, metrics: bool = True) -> "ReplayResult":
-        """Host in, device replay (+ device metrics), host out."""
+    def run(self, stream=None, metrics: bool = True, fetch=None) -> "ReplayResult":
+        """Host in, device replay (+ device metrics), host out.  `fetch`
+        limits the device->host copy to those output arrays (default: all)."""
         din = self.device_inputs()
         dout = self.alloc_outputs(device=True)
         args = self.args(din, dout, D.ptr)
@@ -294,8 +297,10 @@ class ReplayBatch:
             mout = self.alloc_metrics()
             margs = self.metrics_args(din, dout, mout, D.ptr)
             D.check(D.lib().strait_replay_metrics(C.byref(margs), D.stream_handle(stream)))
-            res.update({"m_" + k: D.host(v) for k, v in mout.items()})
-        res.update({k: D.host(v) for k, v in dout.items()})
+            series = ("intf_error", "latency_error", "kernel_overhead")  # per-batch arrays: only on request
+            res.update({"m_" + k: D.host(v) for k, v in mout.items()
+                        if fetch is None or k not in series or "m_" + k in fetch})
+        res.update({k: D.host(v) for k, v in dout.items() if fetch is None or k in fetch or k == "counters"})
         res["pred_state"] = D.host(din["pred_state"])
         res["pred_step"] = D.host(din["pred_step"])
         return ReplayResult(self, res)
