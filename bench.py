@@ -319,9 +319,15 @@ def run_ours(args):
     from paper_2604_28175_b200.predictor import InterferencePredictor
 
     ws, rank, local = dist_env()
+    # one process per GPU; STRAIT_DIST_BACKEND=gloo (test only) lets several ranks share a GPU
+    backend = os.environ.get("STRAIT_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend != "nccl" else local
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     lib = _abi.lib()
 
     soa_h = c3_round(rank, n_segments=args.segments)
