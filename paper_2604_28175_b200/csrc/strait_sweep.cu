@@ -452,7 +452,9 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
       const uint32_t use = (uint32_t)(k / nstages);
       unsigned char* stage = smem + st * W.stage_bytes;
       mbar_wait(&empty[st], (use & 1) ^ 1);
-      if (lane == 0 && use_tmap) {
+      if ((diag & 4) && k >= nstages) {
+        // diagnostic: compute only — after the first fill the stages keep their data
+      } else if (lane == 0 && use_tmap) {
         // packed SoA: two 2-D boxes ([2NM+5] x TT triple fields, [2NM+2] x TP pair fields) + 2 byte arrays
         mbar_expect_tx(&full[st], (uint32_t)L.tx_bytes);
         tma_2d_g2s(stage + L.ent, &ent_map, (int)(tile * tg.TT), 0, &full[st], pol);
