@@ -383,9 +383,20 @@ def run_ours(args):
     kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
     path = SW.last_sweep_path()
 
-    # end to end through the public API: pinned host SoA -> H2D -> round -> D2H decisions
-    pinned = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in soa_h.arrays.items()}
-    h2d = sum(t.numel() * t.element_size() for t in pinned.values())
+    # end to end through the public API with HOST buffers: the round's snapshot as the host
+    # holds it — profile-indexed (microbench.c3_compact: int16 profile rows + the non-derived
+    # fields, and the profile tables) in pinned memory -> H2D into the packed device snapshot ->
+    # strait_sweep_expand -> strait_round -> D2H of every decision output.
+    from paper_2604_28175_b200.microbench import c3_compact
+
+    comp = c3_compact(soa_h)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+    pfields = {k: pin(v) for k, v in comp["fields"].items() if k not in ("ent_row", "cand_row")}
+    prows = {k: pin(comp["fields"][k]) for k in ("ent_row", "cand_row")}
+    ptables = {k: pin(v) for k, v in comp["tables"].items()}
+    dtables = {k: torch.empty_like(v, device="cuda") for k, v in ptables.items()}
+    drows = {k: torch.empty_like(v, device="cuda") for k, v in prows.items()}
+    h2d = sum(t.numel() * t.element_size() for d in (pfields, prows, ptables) for t in d.values())
     host_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in out.items()}
     d2h = sum(t.numel() * t.element_size() for t in host_out.values())
     e2e_ms = []
@@ -393,8 +404,9 @@ def run_ours(args):
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        for k, t in pinned.items():
-            soa.arrays[k].copy_(t, non_blocking=True)
+        for k, t in ptables.items():
+            dtables[k].copy_(t, non_blocking=True)
+        SW.load_compact(soa, pfields, prows, drows, dtables, comp["table_stride"])
         one_round(i, cur, nxt)
         cur, nxt = nxt, cur
         for k, t in out.items():
@@ -440,7 +452,8 @@ def run_ours(args):
         "triples_per_s": ws * soa_h.n_triples * args.steps / (elapsed_ms / 1e3),
         "e2e": {"value": ws * preds / (e2e_step_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step_ms,
-                "path": "pinned host SoA -> H2D -> strait_round (C-ABI) -> D2H decisions"},
+                "path": "pinned profile-indexed snapshot (int16 profile rows + non-derived fields + profile "
+                        "tables) -> H2D -> strait_sweep_expand -> strait_round (C-ABI) -> D2H decisions"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": f"strait_round ({path} sweep path)",
                      "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": kern_ms},

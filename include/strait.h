@@ -183,6 +183,35 @@ typedef struct StraitSweepArgs {
 int strait_sweep(const StraitSweepArgs *args, void *stream);
 
 /*
+ * Profile-indexed snapshots for strait_sweep.  Every co-runner's contribution,
+ * self_compute / self_memory and isolated kernel latency is its profile row at
+ * (model, size) (submit_plan, scheduler.py:295-324), the candidate's likewise,
+ * and a GPU's aggregate / LP aggregate are list-order sums of its running
+ * entries' contributions (runtime.py:104-122).  A host can therefore ship only
+ * row indices plus the non-derived fields; this call fills the derived fields
+ * of `target` (ent_contrib, ent_self_cmp, ent_self_mem, ent_t_kernel, ent_prio,
+ * gpu_agg, gpu_lp_agg, cand_contrib, cand_self_cmp, cand_self_mem, cand_total,
+ * cand_kernel, cand_deadline, cand_prio) exactly as the reference objects hold
+ * them.  row = model * table_stride + size - 1.
+ */
+typedef struct StraitSweepExpandArgs {
+  int32_t table_stride; /* profile rows per model (max batch size) */
+  int32_t pad;
+  const double *thr;      /* [nm][rows] throughput_at(size) */
+  const double *self_cmp; /* [rows] */
+  const double *self_mem; /* [rows] */
+  const double *kernel;   /* [rows] kernel_latency_ms */
+  const double *total;    /* [rows] total_latency_ms */
+  const double *deadline; /* [models] deadline_ms */
+  const int8_t *prio;     /* [models] */
+  const int16_t *ent_row; /* [T] */
+  const int16_t *cand_row; /* [S] */
+  int64_t n_rows;
+} StraitSweepExpandArgs;
+
+int strait_sweep_expand(const StraitSweepExpandArgs *e, const StraitSweepArgs *target, void *stream);
+
+/*
  * R14-R16: sequential online refit, InterferencePredictor.update applied to
  * n samples in order (predictor.py:345-363): Huber-loss gradient under the
  * current parameters, non-finite skip, Adam with the other class's

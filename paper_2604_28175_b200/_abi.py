@@ -111,6 +111,12 @@ class RefitArgs(C.Structure):
     ]
 
 
+class SweepExpandArgs(C.Structure):
+    _fields_ = [("table_stride", C.c_int32), ("pad", C.c_int32), ("thr", _vp), ("self_cmp", _vp),
+                ("self_mem", _vp), ("kernel", _vp), ("total", _vp), ("deadline", _vp), ("prio", _vp),
+                ("ent_row", _vp), ("cand_row", _vp), ("n_rows", C.c_int64)]
+
+
 # field groups of SweepArgs, used by exporters
 SWEEP_CAND_FIELDS = ("cand_contrib", "cand_self_cmp", "cand_self_mem", "cand_total",
                      "cand_kernel", "cand_deadline", "cand_front", "cand_prio")
@@ -150,6 +156,8 @@ def _declare(lib):
     lib.strait_round.argtypes = [C.POINTER(SweepArgs), C.POINTER(RefitArgs), _vp]
     lib.strait_math.restype = C.c_int
     lib.strait_math.argtypes = [C.c_int32, _vp, _vp, C.c_int64, _vp, _vp]
+    lib.strait_sweep_expand.restype = C.c_int
+    lib.strait_sweep_expand.argtypes = [C.POINTER(SweepExpandArgs), C.POINTER(SweepArgs), _vp]
     lib.strait_host_exp.restype = None
     lib.strait_host_exp.argtypes = [_vp, _vp, C.c_int64]
     if hasattr(lib, "strait_replay"):

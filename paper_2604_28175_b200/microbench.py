@@ -126,6 +126,29 @@ def c3_round(round_idx: int, n_segments: int = C3_SEGMENTS, gpus: int = C3_GPUS,
     return soa
 
 
+# fields a profile-indexed snapshot ships (the rest follow from the profile rows)
+COMPACT_FIELDS = ("ent_twa", "ent_deadline_abs", "ent_kstart", "gpu_cap_pct", "gpu_t_avail", "gpu_n_running",
+                  "cand_front")
+
+
+def c3_compact(soa: SweepSoA, profiles=None) -> dict:
+    """Profile-indexed form of a C3 round (strait_sweep_expand): int16 profile
+    rows per co-runner and candidate + the non-derived fields, and the profile
+    tables (row = model * max_batch + size - 1)."""
+    profiles = profiles if profiles is not None else c3_profiles()
+    tab = profile_tables(profiles)
+    bs = tab["total"].shape[1]
+    m = soa.meta
+    out = {k: soa.arrays[k] for k in COMPACT_FIELDS}
+    out["ent_row"] = (m["ent_model"] * bs + m["ent_size"] - 1).astype(np.int16)
+    out["cand_row"] = (m["cand_model"] * bs + m["cand_size"] - 1).astype(np.int16)
+    tables = {"thr": np.ascontiguousarray(tab["thr"].reshape(-1, tab["thr"].shape[2]).T),
+              "self_cmp": tab["cmp"].ravel(), "self_mem": tab["mem"].ravel(), "kernel": tab["kernel"].ravel(),
+              "total": tab["total"].ravel(), "deadline": tab["deadline"], "prio": tab["prio"]}
+    return {"fields": {k: np.ascontiguousarray(v) for k, v in out.items()},
+            "tables": {k: np.ascontiguousarray(v) for k, v in tables.items()}, "table_stride": bs}
+
+
 def c3_feedback(round_idx: int, n: int = C3_FEEDBACK):
     """F feedback samples per round, as the reference's convergence stream
     (test_acceptance.py:280-297): matched-family hidden truth with

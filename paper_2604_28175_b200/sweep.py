@@ -146,5 +146,32 @@ def sweep(soa: SweepSoA, params, effect_cap: float = 50.0, use_violate: bool = T
     return {k: D.host(v) for k, v in out.items()}
 
 
+def expand_args(tables: dict, ent_row: torch.Tensor, cand_row: torch.Tensor, stride: int):
+    from ._abi import SweepExpandArgs
+
+    e = SweepExpandArgs()
+    e.table_stride, e.n_rows = int(stride), int(tables["self_cmp"].numel())
+    for k in ("thr", "self_cmp", "self_mem", "kernel", "total", "deadline", "prio"):
+        setattr(e, k, D.ptr(tables[k]))
+    e.ent_row, e.cand_row = D.ptr(ent_row), D.ptr(cand_row)
+    return e
+
+
+def load_compact(dsoa: SweepSoA, fields: dict, rows: dict, dev_rows: dict, dev_tables: dict, stride: int,
+                 stream=None) -> None:
+    """Fill a device-resident (packed) snapshot from a profile-indexed one
+    (microbench.c3_compact): the non-derived `fields` are copied (H2D from
+    pinned host tensors) straight into their rows of the packed blocks, the
+    int16 profile `rows` into `dev_rows`, and strait_sweep_expand rebuilds
+    every profile-derived field and the list-order aggregates on the device."""
+    for k, v in fields.items():
+        dsoa.arrays[k].copy_(v, non_blocking=True)
+    for k in ("ent_row", "cand_row"):
+        dev_rows[k].copy_(rows[k], non_blocking=True)
+    e = expand_args(dev_tables, dev_rows["ent_row"], dev_rows["cand_row"], stride)
+    a = sweep_args(dsoa, dev_rows["ent_row"], {})  # params unused by the expand
+    D.check(D.lib().strait_sweep_expand(C.byref(e), C.byref(a), D.stream_handle(stream)))
+
+
 def last_sweep_path() -> str:
     return {1: "sync", 2: "tma-bulk", 3: "tma-tensor"}.get(D.lib().strait_last_sweep_path(), "none")

@@ -199,3 +199,33 @@ def test_launch_counter_moves(cuda):
     before = _abi.lib().strait_kernel_launches()
     predict_interference(PredictorParams(), (0.1,) * 5, 0.2, 0.3, 1)
     assert _abi.lib().strait_kernel_launches() == before + 1
+
+
+def test_sweep_expand_profile_indexed_snapshot(cuda):
+    """A profile-indexed C3 snapshot expanded on the device (strait_sweep_expand)
+    is bit-identical to the field-by-field export, and sweeps to the same
+    decisions (the e2e path of bench.py)."""
+    import torch
+
+    from paper_2604_28175_b200 import _device as D
+    from paper_2604_28175_b200 import sweep as SW
+    from paper_2604_28175_b200.microbench import c3_compact, c3_round
+
+    soa = c3_round(3, n_segments=512)
+    full = soa.to_device()
+    comp = c3_compact(soa)
+    blank = soa.like({k: (np.zeros_like(v) if v.dtype != np.int8 else np.zeros_like(v)) for k, v in soa.arrays.items()})
+    dev = blank.to_device()
+    tables = {k: D.dev(v, torch.int8 if v.dtype == np.int8 else torch.float64) for k, v in comp["tables"].items()}
+    rows = {k: torch.from_numpy(comp["fields"][k]) for k in ("ent_row", "cand_row")}
+    dev_rows = {k: D.empty(len(v), torch.int16) for k, v in rows.items()}
+    fields = {k: torch.from_numpy(v) for k, v in comp["fields"].items() if k not in rows}
+    SW.load_compact(dev, fields, rows, dev_rows, tables, comp["table_stride"])
+    for k in full.arrays:
+        np.testing.assert_array_equal(D.host(dev.arrays[k]), D.host(full.arrays[k]), err_msg=k)
+    P = D.dev(np.array([0.1, np.e, 0.0] + [0.1] * 5 + [0.1, 0.1, 0.5, 1.0]))
+    o1, o2 = SW.alloc_outputs(full), SW.alloc_outputs(dev)
+    SW.launch_sweep(full, P, o1)
+    SW.launch_sweep(dev, P, o2)
+    for k in o1:
+        np.testing.assert_array_equal(D.host(o1[k]), D.host(o2[k]), err_msg=k)
