@@ -39,7 +39,7 @@ ARG_ARRAYS = ["cfg", "req_off", "arr_time", "arr_model", "model_req", "mr_off", 
               "dec_time", "dec_pass", "dec_model", "dec_size", "dec_gpu", "dec_est_latency", "dec_intf",
               "b_front", "b_transfer_start", "b_transfer_end", "b_kernel_start", "b_kernel_end", "b_completion",
               "b_work", "b_done_order", "fb_predicted", "fb_actual", "fb_residual", "fb_flags",
-              "cap_time", "cap_gpu", "cap_pct", "counters"]
+              "cap_time", "cap_gpu", "cap_pct", "counters", "order"]
 
 
 class ReplayArgs(C.Structure):

@@ -80,17 +80,22 @@ extern "C" int strait_replay(const StraitReplayArgs* a, void* stream) {
   if (wpc > kMaxWarpsPerCta) wpc = kMaxWarpsPerCta;
   const int64_t want = (a->n_replays + sm_count() - 1) / sm_count();
   if (want < wpc) wpc = (int)(want < 1 ? 1 : want);
+  // variant: the latency kernel while every replay is resident (2 CTAs x 4 warps per
+  // SM), then one warp per CTA so the hardware spreads the (heaviest-first ordered)
+  // replays over SMs and sub-partitions; past that, the 16-replays-per-SM kernel
+  const int minb = replay_occupancy(a->n_replays, wpc);
+  if (minb < 4) wpc = 1;
   cudaStream_t st = (cudaStream_t)stream;
   int rc = STRAIT_EINVAL;
   switch (md.n_metrics) {
-    case 1: rc = launch_replay<1>(*a, st, wpc, per_warp); break;
-    case 2: rc = launch_replay<2>(*a, st, wpc, per_warp); break;
-    case 3: rc = launch_replay<3>(*a, st, wpc, per_warp); break;
-    case 4: rc = launch_replay<4>(*a, st, wpc, per_warp); break;
-    case 5: rc = launch_replay<5>(*a, st, wpc, per_warp); break;
-    case 6: rc = launch_replay<6>(*a, st, wpc, per_warp); break;
-    case 7: rc = launch_replay<7>(*a, st, wpc, per_warp); break;
-    case 8: rc = launch_replay<8>(*a, st, wpc, per_warp); break;
+    case 1: rc = launch_replay<1>(*a, st, wpc, per_warp, minb); break;
+    case 2: rc = launch_replay<2>(*a, st, wpc, per_warp, minb); break;
+    case 3: rc = launch_replay<3>(*a, st, wpc, per_warp, minb); break;
+    case 4: rc = launch_replay<4>(*a, st, wpc, per_warp, minb); break;
+    case 5: rc = launch_replay<5>(*a, st, wpc, per_warp, minb); break;
+    case 6: rc = launch_replay<6>(*a, st, wpc, per_warp, minb); break;
+    case 7: rc = launch_replay<7>(*a, st, wpc, per_warp, minb); break;
+    case 8: rc = launch_replay<8>(*a, st, wpc, per_warp, minb); break;
   }
   return rc;
 }

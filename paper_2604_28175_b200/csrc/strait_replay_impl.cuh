@@ -1182,8 +1182,9 @@ template <int NM, int MINB>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant__ StraitReplayArgs a, int wpc) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int w = threadIdx.x >> 5;
-  const int64_t r = (int64_t)blockIdx.x * wpc + w;
-  if (r >= a.n_replays) return;
+  const int64_t slot_w = (int64_t)blockIdx.x * wpc + w;
+  if (slot_w >= a.n_replays) return;
+  const int64_t r = a.order ? (int64_t)a.order[slot_w] : slot_w;
   const Layout L(a.max_gpus, a.max_concurrency, a.models.n_models, NM);
   unsigned char* base = smem + (size_t)w * L.bytes;
   Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type> S;
@@ -1222,9 +1223,10 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   S.run();
 }
 
-// host side: launch one instantiation (explicitly specialised in strait_replay_nm*.cu)
+// host side: launch one instantiation (explicitly specialised in strait_replay_nm*.cu);
+// minb = 4 selects the 128-register throughput variant, else the latency variant
 template <int NM>
-int launch_replay(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp);
+int launch_replay(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb);
 
 template <int NM, int MINB>
 int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) {
@@ -1237,16 +1239,11 @@ int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_
   return check_launch("strait_replay");
 }
 
-// occupancy variant: env STRAIT_REPLAY_OCC=1|4 forces one; default picks the
-// high-occupancy kernel once there are more replays than the latency kernel
-// can keep resident (2 CTAs x 4 warps per SM).
-int replay_occupancy(int64_t n_replays, int wpc);
-
-#define STRAIT_INSTANTIATE_REPLAY(NMV)                                                                \
-  template <>                                                                                         \
-  int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) { \
-    return replay_occupancy(a.n_replays, wpc) >= 4 ? launch_replay_occ<NMV, 4>(a, st, wpc, smem_per_warp) \
-                                                   : launch_replay_occ<NMV, 1>(a, st, wpc, smem_per_warp); \
+#define STRAIT_INSTANTIATE_REPLAY(NMV)                                                                            \
+  template <>                                                                                                     \
+  int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb) { \
+    return minb >= 4 ? launch_replay_occ<NMV, 4>(a, st, wpc, smem_per_warp)                                      \
+                     : launch_replay_occ<NMV, 1>(a, st, wpc, smem_per_warp);                                      \
   }
 
 }  // namespace rp

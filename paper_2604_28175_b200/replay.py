@@ -199,6 +199,8 @@ class ReplayBatch:
             "pred_state": np.asarray(states, dtype=np.float64).ravel(),
             "pred_step": np.asarray(steps, dtype=np.int64),
             "cfg": (ReplayConfig * self.R)(*cfgs),
+            # launch heaviest replays first so the first CTA wave spreads them over the SMs
+            "order": np.argsort(-np.diff(np.asarray(req_off, dtype=np.int64)), kind="stable").astype(np.int32),
         }
         if generate == "host":
             self.inputs.update(arr_time=np.concatenate(arr_t), arr_model=np.concatenate(arr_m),
