@@ -164,8 +164,12 @@ struct Sim {
   __device__ __forceinline__ int slot_at(int g, int p) const { return slot(g, ORD(p, g)); }
 
   __device__ __forceinline__ void sync() const { __syncwarp(); }
+  // Uniform scalar store: every lane computed v; lane 0 writes it after the warp
+  // has finished its earlier reads of shared state (write-after-read).  Readers
+  // of the new value come after a sync() (read-after-write).
   template <typename T>
-  __device__ __forceinline__ void put(T& ref, T v) const {  // uniform scalar store
+  __device__ __forceinline__ void put(T& ref, T v) const {
+    __syncwarp();
     if (lane == 0) ref = v;
   }
   __device__ __forceinline__ void fail(int code) {
@@ -747,6 +751,7 @@ struct Sim {
     const double start = py_max(now, GD(GD_TAV, g)), end = start + d;
     const double front = arr(req_at(h));
     const double noise = cf->has_noise ? __ldg(&A->noise[base + bid]) : 1.0;  // simulation.py:309-311
+    sync();
     if (lane == 0) {
       QI(QI_HEAD, m) = h + k;  // TaskQueue.pop_front
       QI(QI_FGEN, m) = QI(QI_FGEN, m) + 1;
@@ -887,6 +892,7 @@ struct Sim {
       fail(STRAIT_EINVAL);
       return;
     }
+    sync();
     if (lane == 0) {
       // calibrate (pcie.py:36-53): FIFO => the oldest reservation is this batch's
       const int ph = GI(GI_PHEAD, g);
@@ -926,6 +932,7 @@ struct Sim {
     const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s), prio = SB(SB_PRIO, s);
     const int bid = SI(SI_BID, s), req0 = SI(SI_REQ0, s);
     bool ok = true;
+    sync();
     if (lane == 0) ok = ex_consume(s, now);
     fail_any(!ok, STRAIT_EORDER);
     sync();
@@ -1100,6 +1107,7 @@ struct Sim {
         bt = __longlong_as_double((long long)(((unsigned long long)m0 << 32) | m1));
         bi = __shfl_sync(kFull, bi, __ffs(__ballot_sync(kFull, c)) - 1);
       }
+      sync();  // the scan's reads of the event homes complete before any handler writes them
       const int kind = (int)(bk >> 56);
       const double now = bt;
       ++c_events;
