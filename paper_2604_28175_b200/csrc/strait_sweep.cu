@@ -586,16 +586,11 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
       s_adm[pl] = admitted;
     }
 
-    // ---- 3. last warp of the tile: best_for argmin per segment ----
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      __threadfence_block();
-      last = atomicAdd((int*)(stage + W.cnt), 1) == 7;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
+    // ---- 3. best_for argmin per segment, by the group's warp 0 after a named
+    // barrier among the group's 8 consumer warps (the producer / refit warps never join it)
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(8 * 32) : "memory");
+    const int last = wg == 0;
     if (last) {
-      __threadfence_block();
       for (int q = 0; q < spb; ++q) {
         ArgminKey key{INT_MAX, 0.0, INT_MAX, 0.0};
         for (int gg = lane; gg < G; gg += 32) {
@@ -619,7 +614,6 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
           a.seg_intf[s] = bg >= 0 ? s_intf[q * G + bg] : nan;
         }
       }
-      if (lane == 0) *(int*)(stage + W.cnt) = 0;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
