@@ -353,13 +353,14 @@ struct BulkCopy {
 template <int NM>
 struct WsLayout {
   StageLayout<NM> st;
-  size_t res_lat, res_intf, res_adm, cnt, stage_bytes;
+  size_t res_lat, res_intf, res_adm, res_viol, cnt, stage_bytes;
   size_t pred, full, empty, refit, copies, etab, bytes;
   __host__ __device__ WsLayout(const TileGeom& t, int nstages) : st(t) {
     res_lat = st.bytes;
     res_intf = res_lat + (size_t)t.TP * 8;
     res_adm = res_intf + (size_t)t.TP * 8;
-    cnt = align_up(res_adm + t.TP, 16);
+    res_viol = res_adm + t.TP;  // per pair: some co-runner projection violates (phase 1)
+    cnt = align_up(res_viol + t.TP, 16);
     stage_bytes = align_up(cnt + 16, 128);
     pred = stage_bytes * nstages;
     full = align_up(pred + sizeof(Pred<NM>), 16);
@@ -549,46 +550,56 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
     unsigned vbits = viol ? 1u : 0u;
 #pragma unroll
     for (int o = C / 2; o > 0; o >>= 1) vbits |= __shfl_xor_sync(0xffffffffu, vbits, o, C);
+    uint8_t* s_viol = (uint8_t*)(stage + W.res_viol);
+    if (active && c == 0) s_viol[pl] = vbits != 0;
+    // all of the tile's projections are published (named barrier of the group's 8 consumer warps)
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(8 * 32) : "memory");
 
-    // ---- 2. pair: LP cap + check_meet on the leader lane ----
-    if (active && c == 0) {
-      uint8_t flags = 0;
-      double lat = nan, intf = nan;
-      bool admitted = false;
-      if (nrun < a.concurrency_limit) {
-        flags |= STRAIT_PAIR_HAS_SLOT;
-        bool violate = vbits != 0;
-        if (cprio == 1) {
-          const double cap_fraction = pair[(2 * NM) * TP + pl] / 100.0;
+    // ---- 2. pair: LP cap + check_meet, one lane per pair on the first ceil(TP/32) warps ----
+    const int npw = (TP + 31) >> 5;
+    if (wg < npw) {
+      const int pp = wg * 32 + lane;
+      if (pp < TP) {
+        const int psl = pp / G;
+        const int pn = ((const int8_t*)(stage + L.nrun))[pp];
+        const int pprio = ((const int8_t*)(stage + L.cprio))[4 * psl + (int)((tile * spb + psl) & 3)];
+        uint8_t flags = 0;
+        double lat = nan, intf = nan;
+        bool admitted = false;
+        if (pn < a.concurrency_limit) {  // has_slot (runtime.py:101-102)
+          flags |= STRAIT_PAIR_HAS_SLOT;
+          bool violate = s_viol[pp] != 0;
+          if (pprio == 1) {  // LOW candidate vs the AIMD cap (scheduler.py:130-135)
+            const double cap_fraction = pair[(2 * NM) * TP + pp] / 100.0;  // runtime.py:39-40
 #pragma unroll
-          for (int m = 0; m < NM; ++m)
-            if (pair[(NM + m) * TP + pl] + cand[m * spb + sl] > cap_fraction) violate = true;
+            for (int m = 0; m < NM; ++m)
+              if (pair[(NM + m) * TP + pp] + cand[m * spb + psl] > cap_fraction) violate = true;
+          }
+          if (violate) flags |= STRAIT_PAIR_VIOLATE;
+          double assumed[NM];  // check_meet: half the GPU aggregate (scheduler.py:178)
+#pragma unroll
+          for (int m = 0; m < NM; ++m) assumed[m] = 0.5 * pair[m * TP + pp];
+          intf = pr.predict(assumed, cand[(NM + 0) * spb + psl], cand[(NM + 1) * spb + psl], pprio);
+          const double wait = py_max(0.0, pair[(2 * NM + 1) * TP + pp] - now);  // pcie.py:21-23
+          lat = cand[(NM + 2) * spb + psl] + wait + (intf - 1.0) * cand[(NM + 3) * spb + psl] +
+                (now - cand[(NM + 4) * spb + psl]);
+          const bool ok = lat <= cand[(NM + 5) * spb + psl];
+          if (ok) flags |= STRAIT_PAIR_MEET;
+          admitted = !(a.use_violate && violate) && !(a.use_meet && !ok);
+          if (admitted) flags |= STRAIT_PAIR_FEASIBLE;
         }
-        if (violate) flags |= STRAIT_PAIR_VIOLATE;
-        double assumed[NM];
-#pragma unroll
-        for (int m = 0; m < NM; ++m) assumed[m] = 0.5 * pair[m * TP + pl];
-        intf = pr.predict(assumed, cand[(NM + 0) * spb + sl], cand[(NM + 1) * spb + sl], cprio);
-        const double wait = py_max(0.0, pair[(2 * NM + 1) * TP + pl] - now);
-        lat = cand[(NM + 2) * spb + sl] + wait + (intf - 1.0) * cand[(NM + 3) * spb + sl] +
-              (now - cand[(NM + 4) * spb + sl]);
-        const bool ok = lat <= cand[(NM + 5) * spb + sl];
-        if (ok) flags |= STRAIT_PAIR_MEET;
-        admitted = !(a.use_violate && violate) && !(a.use_meet && !ok);
-        if (admitted) flags |= STRAIT_PAIR_FEASIBLE;
+        const int64_t p = tile * TP + pp;
+        if (a.pair_flags) a.pair_flags[p] = flags;
+        if (a.pair_latency) __stcs(a.pair_latency + p, lat);
+        if (a.pair_intf) __stcs(a.pair_intf + p, intf);
+        s_lat[pp] = lat;
+        s_intf[pp] = intf;
+        s_adm[pp] = admitted;
       }
-      const int64_t p = tile * TP + pl;
-      if (a.pair_flags) a.pair_flags[p] = flags;
-      if (a.pair_latency) __stcs(a.pair_latency + p, lat);
-      if (a.pair_intf) __stcs(a.pair_intf + p, intf);
-      s_lat[pl] = lat;
-      s_intf[pl] = intf;
-      s_adm[pl] = admitted;
+      if (npw > 1) asm volatile("bar.sync %0, %1;" ::"r"(3 + group), "r"(npw * 32) : "memory");
     }
 
-    // ---- 3. best_for argmin per segment, by the group's warp 0 after a named
-    // barrier among the group's 8 consumer warps (the producer / refit warps never join it)
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(8 * 32) : "memory");
+    // ---- 3. warp 0: best_for argmin per segment ----
     const int last = wg == 0;
     if (last) {
       for (int q = 0; q < spb; ++q) {
