@@ -25,3 +25,23 @@ def test_reference_suite_against_mirror(module, tmp_path):
                        timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/pkg/configs"), reason="reference configs not mounted")
+@pytest.mark.parametrize("name,case", [("demo.yaml", "demo"), ("overload.yaml", "overload")])
+def test_shipped_yaml_configs_load_to_the_golden_inputs(name, case):
+    """config.load_config on the reference's shipped YAML gives exactly the
+    replay inputs of the restated config the golden replays were made from."""
+    import numpy as np
+
+    from paper_2604_28175_b200.config import load_config
+    from paper_2604_28175_b200.replay import ReplayBatch, ReplaySpec
+    from replay_cases import case_config
+
+    a = ReplayBatch([ReplaySpec(load_config(os.path.join("/root/reference/pkg/configs", name)))]).host_inputs()
+    b = ReplayBatch([ReplaySpec(case_config(case))]).host_inputs()
+    for k in b:
+        if k == "cfg":
+            assert bytes(a[k]) == bytes(b[k])
+        else:
+            np.testing.assert_array_equal(a[k], b[k], err_msg=k)
