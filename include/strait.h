@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define STRAIT_ABI_VERSION 1
+#define STRAIT_ABI_VERSION 2
 
 /* error codes; the Python mirror maps them to the reference's exceptions */
 #define STRAIT_OK 0
@@ -50,6 +50,11 @@ extern "C" {
 #define STRAIT_PAIR_FEASIBLE 8u /* admitted by best_for under the flags   (scheduler.py:263-280) */
 
 int strait_abi_version(void);
+/* sizeof of each ABI struct, so bindings can verify their mirrors (HOST only):
+ * 0 StraitSweepArgs, 1 StraitSweepExpandArgs, 2 StraitRefitArgs, 3 StraitReplayModels,
+ * 4 StraitReplayConfig, 5 StraitReplayArgs, 6 StraitTraceRec, 7 StraitMetricsArgs,
+ * 8 StraitStreamSpec; -1 for an unknown id */
+int64_t strait_struct_size(int32_t id);
 const char *strait_last_error(void);
 /* number of device kernels this library launched since load (evidence counter) */
 int64_t strait_kernel_launches(void);

@@ -14,6 +14,7 @@ import threading
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_strait.so")
 
+ABI_VERSION = 2  # include/strait.h STRAIT_ABI_VERSION
 STRAIT_OK = 0
 STRAIT_EINVAL = 1
 STRAIT_ERUNTIME = 2
@@ -132,6 +133,8 @@ _lock = threading.Lock()
 
 def _declare(lib):
     lib.strait_abi_version.restype = C.c_int
+    lib.strait_struct_size.restype = C.c_int64
+    lib.strait_struct_size.argtypes = [C.c_int32]
     lib.strait_last_error.restype = C.c_char_p
     lib.strait_kernel_launches.restype = C.c_int64
     lib.strait_predict.restype = C.c_int
@@ -183,7 +186,7 @@ def lib():
                 )
             handle = C.CDLL(LIB_PATH)
             _declare(handle)
-            if handle.strait_abi_version() != 1:
+            if handle.strait_abi_version() != ABI_VERSION:
                 raise StraitUnavailable("strait ABI version mismatch")
             _lib = handle
     return _lib

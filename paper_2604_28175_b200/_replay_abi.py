@@ -3,12 +3,14 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
+
 from ._abi import MAX_METRICS
 
 _vp = C.c_void_p
 
 RC = dict(ERROR=0, BATCHES=1, COMPLETED=2, PASSES=3, CAP_ROWS=4, EVENTS=5, HP_ARR=6, LP_ARR=7, HP_VIOL=8,
-          LP_VIOL=9, HP_DROP=10, LP_DROP=11, RESOLVED=12)
+          LP_VIOL=9, HP_DROP=10, LP_DROP=11, RESOLVED=12, TRACE=13)
 RC_N = 16
 
 
@@ -39,14 +41,21 @@ ARG_ARRAYS = ["cfg", "req_off", "arr_time", "arr_model", "model_req", "mr_off", 
               "dec_time", "dec_pass", "dec_model", "dec_size", "dec_gpu", "dec_est_latency", "dec_intf",
               "b_front", "b_transfer_start", "b_transfer_end", "b_kernel_start", "b_kernel_end", "b_completion",
               "b_work", "b_done_order", "fb_predicted", "fb_actual", "fb_residual", "fb_flags",
-              "cap_time", "cap_gpu", "cap_pct", "counters", "order"]
+              "cap_time", "cap_gpu", "cap_pct", "counters", "order", "trace"]
 
 
 class ReplayArgs(C.Structure):
     _fields_ = [("n_replays", C.c_int32), ("cap_rows_max", C.c_int32), ("n_bc", C.c_int32),
-                ("max_gpus", C.c_int32), ("max_concurrency", C.c_int32), ("pad", C.c_int32 * 3),
+                ("max_gpus", C.c_int32), ("max_concurrency", C.c_int32), ("trace_max", C.c_int32),
+                ("pad", C.c_int32 * 2),
                 ("models", ReplayModels)] + [(k, _vp) for k in ARG_ARRAYS]
 
+
+# StraitTraceRec and the STRAIT_TR_* event codes
+TRACE_DTYPE = np.dtype([("time", "<f8"), ("x", "<f8", (3,)), ("request", "<i8"), ("batch", "<i4"),
+                        ("gpu", "<i2"), ("event", "i1"), ("size", "i1")])
+assert TRACE_DTYPE.itemsize == 48
+TR = dict(ARRIVAL=0, SUBMIT=1, DROP=2, KSTART=3, KDONE=4, TICK=5, RESET=6, SEGMENT=7)
 
 MS_N = 5
 METRIC_ARRAYS = ["window_ms", "req_off", "arr_time", "arr_model", "model_prio", "req_status", "req_violated",

@@ -8,6 +8,7 @@
 #include <cstdio>
 
 #include "strait_capi.cuh"
+#include "../../include/strait_replay.h"
 
 namespace {
 thread_local char g_err[1024] = "";
@@ -34,6 +35,20 @@ int check_launch(const char* what) {
 }  // namespace strait
 
 extern "C" int strait_abi_version(void) { return STRAIT_ABI_VERSION; }
+extern "C" int64_t strait_struct_size(int32_t id) {
+  switch (id) {
+    case 0: return sizeof(StraitSweepArgs);
+    case 1: return sizeof(StraitSweepExpandArgs);
+    case 2: return sizeof(StraitRefitArgs);
+    case 3: return sizeof(StraitReplayModels);
+    case 4: return sizeof(StraitReplayConfig);
+    case 5: return sizeof(StraitReplayArgs);
+    case 6: return sizeof(StraitTraceRec);
+    case 7: return sizeof(StraitMetricsArgs);
+    case 8: return sizeof(StraitStreamSpec);
+  }
+  return -1;
+}
 extern "C" const char* strait_last_error(void) { return g_err; }
 extern "C" int64_t strait_kernel_launches(void) { return g_launches.load(); }
 

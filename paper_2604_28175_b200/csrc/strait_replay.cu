@@ -75,6 +75,7 @@ extern "C" int strait_replay(const StraitReplayArgs* a, void* stream) {
     if (!p) return set_error(STRAIT_EINVAL, "strait_replay: null buffer");
   if (a->cap_rows_max > 0 && (!a->cap_time || !a->cap_gpu || !a->cap_pct))
     return set_error(STRAIT_EINVAL, "strait_replay: null cap-row buffer");
+  if (a->trace && a->trace_max < 0) return set_error(STRAIT_EINVAL, "strait_replay: trace_max < 0");
   // warps per CTA: enough CTAs to cover the SMs first, then pack up to the smem budget
   int wpc = (int)(kSmemBudget / per_warp);
   if (wpc > kMaxWarpsPerCta) wpc = kMaxWarpsPerCta;
@@ -83,7 +84,8 @@ extern "C" int strait_replay(const StraitReplayArgs* a, void* stream) {
   // variant: the latency kernel while every replay is resident (2 CTAs x 4 warps per
   // SM), then one warp per CTA so the hardware spreads the (heaviest-first ordered)
   // replays over SMs and sub-partitions; past that, the 16-replays-per-SM kernel
-  const int minb = replay_occupancy(a->n_replays, wpc);
+  // a traced launch (event log) always runs the latency variant with the log compiled in
+  const int minb = a->trace ? 0 : replay_occupancy(a->n_replays, wpc);
   if (minb < 4) wpc = 1;
   cudaStream_t st = (cudaStream_t)stream;
   int rc = STRAIT_EINVAL;

@@ -93,7 +93,7 @@ enum { QI_HEAD, QI_TAIL, QI_FGEN, QI_TGEN, QI_EGEN, QI_ORD, QI_N };
 
 struct Layout {
   int G, C, M, NM, S, NE;
-  size_t P, sd, gd, ed, ek, qd, si, gi, qi, sb, go, qb, bytes;
+  size_t P, sd, gd, ed, ek, qd, qf, si, gi, qi, sb, go, qb, bytes;
   __host__ __device__ static int sd_fields(int nm) { return SD_VL + 4 * nm; }
   __host__ __device__ static int gd_fields(int nm, int c) { return GD_AGG + 2 * nm + c; }
   __host__ __device__ Layout(int g, int c, int m, int nm) : G(g), C(c), M(m), NM(nm) {
@@ -111,6 +111,7 @@ struct Layout {
     ed = take(8 * (size_t)NE);
     ek = take(8 * (size_t)NE);
     qd = take(8 * (size_t)M);
+    qf = take(8 * (size_t)M);
     si = take(4 * (size_t)SI_N * S);
     gi = take(4 * (size_t)GI_N * G);
     qi = take(4 * (size_t)QI_N * M);
@@ -121,7 +122,7 @@ struct Layout {
   }
 };
 
-template <int NM, typename MathT>
+template <int NM, typename MathT, bool TR>
 struct Sim {
   static constexpr int NP = NM + 7;
   static constexpr int SD_ACC = SD_VL + NM;   // timeline integral
@@ -138,6 +139,7 @@ struct Sim {
   int64_t r, base, N;     // request range [base, base + N)
   // ---- shared-memory state: grouped field arrays of this warp's slice
   double *P, *sd, *gd, *ed, *qd;
+  double* qf;  // front arrival time of each non-empty queue (cache of arr(model_req[head]))
   unsigned long long* ek;
   int *si, *gi, *qi;
   int8_t *sb, *go, *qb;
@@ -151,6 +153,7 @@ struct Sim {
   double last_reset;
   int64_t next_arr, resolved;
   int64_t c_batches, c_completed, c_passes, c_cap_rows, c_events, c_hp_viol, c_lp_viol, c_hp_drop, c_lp_drop;
+  int64_t c_trace;  // trace records produced (TR)
 
   // ------------------------------------------------------------ accessors
   __device__ __forceinline__ double& SD(int f, int s) const { return sd[f * S + s]; }
@@ -195,7 +198,7 @@ struct Sim {
   __device__ __forceinline__ int64_t req_at(int pos) const { return __ldg(&A->model_req[pos]); }
   __device__ __forceinline__ double arr(int64_t gidx) const { return __ldg(&A->arr_time[gidx]); }
   __device__ __forceinline__ int q_len(int m) const { return QI(QI_TAIL, m) - QI(QI_HEAD, m); }
-  __device__ __forceinline__ double front_arrival(int m) const { return arr(req_at(QI(QI_HEAD, m))); }
+  __device__ __forceinline__ double front_arrival(int m) const { return qf[m]; }
 
   __device__ __forceinline__ void push_event(int i, double t, int kind) {  // Simulation._push (simulation.py:202-205)
     ++seq;
@@ -213,6 +216,31 @@ struct Sim {
       A->cap_time[o] = t;
       A->cap_gpu[o] = (int16_t)g;
       A->cap_pct[o] = pct;
+    }
+  }
+
+  // Simulation._trace (simulation.py:207-218), TR only: record i of this replay's log
+  __device__ __forceinline__ void trace_put(int64_t i, int ev, double t, int gpu, int bid, int64_t req, int size,
+                                            double x0, double x1, double x2) const {
+    if (i < A->trace_max) {
+      StraitTraceRec* o = A->trace + r * (int64_t)A->trace_max + i;
+      o->time = t;
+      o->x[0] = x0;
+      o->x[1] = x1;
+      o->x[2] = x2;
+      o->request = req;
+      o->batch = bid;
+      o->gpu = (int16_t)gpu;
+      o->event = (int8_t)ev;
+      o->size = (int8_t)size;
+    }
+  }
+  // one record with uniform fields, written by lane 0
+  __device__ __forceinline__ void trace1(int ev, double t, int gpu = -1, int bid = -1, int64_t req = -1, int size = 0,
+                                         double x0 = 0.0, double x1 = 0.0, double x2 = 0.0) {
+    if constexpr (TR) {
+      if (lane == 0) trace_put(c_trace, ev, t, gpu, bid, req, size, x0, x1, x2);
+      ++c_trace;
     }
   }
 
@@ -329,10 +357,13 @@ struct Sim {
     int s = -1;
     bool started = false, ok = true;
     double eta = 0.0;
+    double seg_d = 0.0, seg_slow = 0.0;
     if (lane < n) {
       s = slot_at(g, lane);
       started = SB(SB_STARTED, s);
       if (started) {
+        seg_d = now - SD(SD_LAST, s);
+        seg_slow = SD(SD_SLOW, s);
         ok = ex_consume(s, now);
         const double slow = gt_slowdown(s);
         SD(SD_SLOW, s) = slow;
@@ -346,6 +377,14 @@ struct Sim {
       ek[s] = ((unsigned long long)kKC << 56) | q;
     }
     seq += __popc(mask);
+    if constexpr (TR) {  // ExecutionState.segments: (d, slowdown) for every d > 0 advance
+      const bool seg = started && seg_d > 0;
+      const unsigned sm = __ballot_sync(kFull, seg);
+      if (seg)
+        trace_put(c_trace + __popc(sm & ((1u << lane) - 1)), STRAIT_TR_SEGMENT, now, g, SI(SI_BID, s), -1, 0, seg_d,
+                  seg_slow, 0.0);
+      c_trace += __popc(sm);
+    }
     sync();
     fail_any(!ok, STRAIT_EORDER);
   }
@@ -385,6 +424,10 @@ struct Sim {
       const unsigned mask = __ballot_sync(kFull, changed);
       if (changed) cap_row_at(c_cap_rows + __popc(mask & ((1u << lane) - 1)), now, g, cap);
       c_cap_rows += __popc(mask);
+      if constexpr (TR) {  // "aimd_reset" rows, GPU order (simulation.py:226-229)
+        if (changed) trace_put(c_trace + __popc(mask & ((1u << lane) - 1)), STRAIT_TR_RESET, now, g, -1, -1, 0, cap, 0.0, 0.0);
+        c_trace += __popc(mask);
+      }
     }
     sync();
   }
@@ -724,11 +767,16 @@ struct Sim {
       A->req_completion[gidx] = __longlong_as_double(0x7ff8000000000000LL);
       A->req_batch[gidx] = -1;
     }
+    if constexpr (TR) {  // "drop" rows in queue order (simulation.py:353-355)
+      for (int i = lane; i < ndrop; i += 32) trace_put(c_trace + i, STRAIT_TR_DROP, now, -1, -1, req_at(h + i), 0, 0.0, 0.0, 0.0);
+      c_trace += ndrop;
+    }
     resolved += ndrop;
     if (mprio(m) == 0) c_hp_drop += ndrop, c_hp_viol += ndrop;
     else c_lp_drop += ndrop, c_lp_viol += ndrop;
     put(QI(QI_HEAD, m), h + ndrop);
     put(QI(QI_FGEN, m), QI(QI_FGEN, m) + 1);
+    if (h + ndrop < t) put(qf[m], arr(req_at(h + ndrop)));
     sync();
     if (mprio(m) == 0) signal_hp(-1, now);  // simulation.py:352-357
   }
@@ -749,11 +797,13 @@ struct Sim {
     const double d = tab_transfer(m, k);
     if (!(d > 0)) fail(STRAIT_EINVAL);  // PcieLinkState.reserve (pcie.py:28-29)
     const double start = py_max(now, GD(GD_TAV, g)), end = start + d;
-    const double front = arr(req_at(h));
+    const double front = qf[m];
+    const double next_front = h + k < QI(QI_TAIL, m) ? arr(req_at(h + k)) : 0.0;
     const double noise = cf->has_noise ? __ldg(&A->noise[base + bid]) : 1.0;  // simulation.py:309-311
     sync();
     if (lane == 0) {
       QI(QI_HEAD, m) = h + k;  // TaskQueue.pop_front
+      qf[m] = next_front;
       QI(QI_FGEN, m) = QI(QI_FGEN, m) + 1;
       GD(GD_TAV, g) = end;
       GD(GD_PEND + (GI(GI_PHEAD, g) + GI(GI_PN, g)) % C, g) = end;
@@ -787,6 +837,7 @@ struct Sim {
     push_event(s, end, kTC);
     sync();
     recompute(g, now);
+    trace1(STRAIT_TR_SUBMIT, now, g, bid, -1, k, start, end, plan.lat);  // simulation.py:321-328
     if (lane == 0) {
       const int64_t o = base + bid;
       A->dec_time[o] = now;
@@ -923,6 +974,7 @@ struct Sim {
     }
     sync();
     push_event(s, SD(SD_LAST, s) + SD(SD_REM, s) * SD(SD_SLOW, s), kKC);
+    trace1(STRAIT_TR_KSTART, now, g, SI(SI_BID, s), -1, 0, SD(SD_SLOW, s));  // simulation.py:391-394
     sync();
   }
 
@@ -932,8 +984,10 @@ struct Sim {
     const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s), prio = SB(SB_PRIO, s);
     const int bid = SI(SI_BID, s), req0 = SI(SI_REQ0, s);
     bool ok = true;
+    const double seg_d = now - SD(SD_LAST, s), seg_slow = SD(SD_SLOW, s);
     sync();
     if (lane == 0) ok = ex_consume(s, now);
+    if (seg_d > 0) trace1(STRAIT_TR_SEGMENT, now, g, bid, -1, 0, seg_d, seg_slow);  // ExecutionState.finish
     fail_any(!ok, STRAIT_EORDER);
     sync();
     const double measured = now - SD(SD_KS, s);
@@ -995,6 +1049,7 @@ struct Sim {
     ++done_order;
     ++c_completed;
     recompute(g, now);
+    trace1(STRAIT_TR_KDONE, now, g, bid, -1, 0, measured, actual);  // simulation.py:454-457
     if (prio == 0 && nviol) signal_hp(g, now);  // simulation.py:458-459
   }
 
@@ -1125,7 +1180,11 @@ struct Sim {
         const int t = QI(QI_TAIL, m);
         if (req_at(t) != gidx) fail(STRAIT_EINVAL);  // per-model arrivals must pop in k order
         put(QI(QI_TAIL, m), t + 1);
-        if (t + 1 - QI(QI_HEAD, m) == 1) put(QI(QI_FGEN, m), QI(QI_FGEN, m) + 1);  // TaskQueue.push
+        if (t + 1 - QI(QI_HEAD, m) == 1) {  // TaskQueue.push into an empty queue: new front
+          put(QI(QI_FGEN, m), QI(QI_FGEN, m) + 1);
+          put(qf[m], now);
+        }
+        trace1(STRAIT_TR_ARRIVAL, now, -1, -1, gidx);  // simulation.py:368
         sync();
         pass = q_len(m) == mmaxb(m);
         post_timeout = m;
@@ -1144,6 +1203,7 @@ struct Sim {
         clear_event(bi);
         sync();
         on_tick_advance(now);
+        trace1(STRAIT_TR_TICK, now);  // simulation.py:468
         pass = true;
         post_tick = true;
       }
@@ -1179,6 +1239,7 @@ struct Sim {
       c[STRAIT_RC_HP_DROP] = c_hp_drop;
       c[STRAIT_RC_LP_DROP] = c_lp_drop;
       c[STRAIT_RC_RESOLVED] = resolved;
+      c[STRAIT_RC_TRACE] = c_trace;
     }
   }
 };
@@ -1186,7 +1247,7 @@ struct Sim {
 // MINB = minimum resident CTAs of 4 warps per SM: 1 lets ptxas keep the whole
 // replay state in registers (latency: few replays), 4 caps it at 128 registers
 // for 16 resident replays per SM (throughput: replay sweeps).
-template <int NM, int MINB>
+template <int NM, int MINB, bool TR>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant__ StraitReplayArgs a, int wpc) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int w = threadIdx.x >> 5;
@@ -1195,7 +1256,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   const int64_t r = a.order ? (int64_t)a.order[slot_w] : slot_w;
   const Layout L(a.max_gpus, a.max_concurrency, a.models.n_models, NM);
   unsigned char* base = smem + (size_t)w * L.bytes;
-  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type> S;
+  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type, TR> S;
   S.A = &a;
   S.cf = a.cfg + r;
   S.lane = threadIdx.x & 31;
@@ -1216,6 +1277,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   S.ed = (double*)(base + L.ed);
   S.ek = (unsigned long long*)(base + L.ek);
   S.qd = (double*)(base + L.qd);
+  S.qf = (double*)(base + L.qf);
   S.si = (int*)(base + L.si);
   S.gi = (int*)(base + L.gi);
   S.qi = (int*)(base + L.qi);
@@ -1226,32 +1288,34 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   S.lp_allowance = S.cf->reactive_default;
   S.last_reset = 0.0;
   S.resolved = 0;
-  S.c_batches = S.c_completed = S.c_passes = S.c_events = 0;
+  S.c_batches = S.c_completed = S.c_passes = S.c_events = S.c_trace = 0;
   S.c_hp_viol = S.c_lp_viol = S.c_hp_drop = S.c_lp_drop = 0;
   S.run();
 }
 
 // host side: launch one instantiation (explicitly specialised in strait_replay_nm*.cu);
-// minb = 4 selects the 128-register throughput variant, else the latency variant
+// minb = 4 selects the 128-register throughput variant, 0 the traced latency variant,
+// else the latency variant
 template <int NM>
 int launch_replay(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb);
 
-template <int NM, int MINB>
+template <int NM, int MINB, bool TR>
 int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) {
   const size_t smem = smem_per_warp * wpc;
-  if (cudaFuncSetAttribute(replay_kernel<NM, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  if (cudaFuncSetAttribute(replay_kernel<NM, MINB, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return set_error(STRAIT_ECUDA, "strait_replay: cannot reserve %zu B of shared memory", smem);
   const unsigned grid = (unsigned)((a.n_replays + wpc - 1) / wpc);
-  replay_kernel<NM, MINB><<<grid, 32 * wpc, smem, st>>>(a, wpc);
+  replay_kernel<NM, MINB, TR><<<grid, 32 * wpc, smem, st>>>(a, wpc);
   return check_launch("strait_replay");
 }
 
 #define STRAIT_INSTANTIATE_REPLAY(NMV)                                                                            \
   template <>                                                                                                     \
   int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb) { \
-    return minb >= 4 ? launch_replay_occ<NMV, 4>(a, st, wpc, smem_per_warp)                                      \
-                     : launch_replay_occ<NMV, 1>(a, st, wpc, smem_per_warp);                                      \
+    return minb >= 4   ? launch_replay_occ<NMV, 4, false>(a, st, wpc, smem_per_warp)                            \
+           : minb == 0 ? launch_replay_occ<NMV, 1, true>(a, st, wpc, smem_per_warp)                             \
+                       : launch_replay_occ<NMV, 1, false>(a, st, wpc, smem_per_warp);                           \
   }
 
 }  // namespace rp

@@ -19,7 +19,7 @@ import torch
 
 from . import _device as D
 from ._replay_abi import (ARG_ARRAYS, METRIC_OUTPUTS, MS_N, POLICY_CODES, RC, RC_N, MetricsArgs, ReplayArgs,
-                          ReplayConfig, ReplayModels)
+                          ReplayConfig, ReplayModels, TRACE_DTYPE)
 from .config import ExperimentConfig
 from .domain import PriorityLevel
 from .predictor import InterferencePredictor, PredictorParams, bias_correction_tables
@@ -122,9 +122,13 @@ def replay_config(cfg: ExperimentConfig, pred: InterferencePredictor) -> ReplayC
 class ReplayBatch:
     """Host inputs of a batch of replays sharing one profile set."""
 
-    def __init__(self, specs: Sequence[ReplaySpec], cap_rows_max: Optional[int] = None, generate: str = "host"):
+    def __init__(self, specs: Sequence[ReplaySpec], cap_rows_max: Optional[int] = None, generate: str = "host",
+                 trace: bool = False, trace_max: Optional[int] = None):
         """generate="host": draw the arrival / noise streams with numpy here;
-        generate="device": draw the same streams on the GPU (devgen.py)."""
+        generate="device": draw the same streams on the GPU (devgen.py).
+        trace=True also records the event log (SimResult.trace_rows) and the
+        execution segments; `trace_max` records per replay (default: an
+        estimate, grown and re-run if a replay overflows it)."""
         if not specs:
             raise ValueError("empty replay batch")
         if generate not in ("host", "device"):
@@ -193,6 +197,12 @@ class ReplayBatch:
                 s.config.n_gpus * (2 * (int(s.config.workload.duration_ms / s.config.aimd.interval_ms) + 400) + 3)
                 for s in self.specs)
         self.cap_rows_max = int(cap_rows_max)
+        self.trace = bool(trace)
+        if trace_max is None:  # arrivals + drops + 3 rows per batch + segments + ticks / resets
+            n_max = int(np.max(np.diff(np.asarray(req_off, dtype=np.int64)))) if len(req_off) > 1 else 0
+            trace_max = max(6 * n_max + (int(s.config.workload.duration_ms / s.config.aimd.interval_ms) + 8)
+                            * (s.config.n_gpus + 1) for s in self.specs) + 256
+        self.trace_max = int(min(trace_max, 2**31 - 1)) if self.trace else 0
         self.inputs = {
             "req_off": np.asarray(req_off, dtype=np.int64), "mr_off": np.asarray(mr_off, dtype=np.int64),
             "bc1": bc1, "bc2": bc2,
@@ -215,6 +225,9 @@ class ReplayBatch:
                 out[k] = D.empty(sizes[per], getattr(torch, np.dtype(dt).name))
             else:
                 out[k] = np.zeros(sizes[per], dtype=dt)
+        if self.trace:
+            nbytes = max(self.R * self.trace_max, 1) * TRACE_DTYPE.itemsize
+            out["trace"] = D.empty(nbytes, torch.uint8) if device else np.zeros(nbytes, np.uint8)
         return out
 
     def args(self, inputs: dict, outputs: dict, ptr) -> ReplayArgs:
@@ -222,6 +235,7 @@ class ReplayBatch:
         a.n_replays, a.cap_rows_max, a.n_bc = self.R, self.cap_rows_max, len(self.inputs["bc1"])
         a.max_gpus = max(s.config.n_gpus for s in self.specs)
         a.max_concurrency = max(s.config.concurrency_limit for s in self.specs)
+        a.trace_max = self.trace_max
         t = self.tab
         md = a.models
         md.n_models, md.n_metrics, md.stride = t["M"], t["nm"], t["B"]
@@ -229,6 +243,8 @@ class ReplayBatch:
                   "self_mem", "throughput"):
             setattr(md, k, ptr(inputs["tab_" + k]))
         for k in ARG_ARRAYS:
+            if k == "trace" and "trace" not in outputs:
+                continue  # NULL: no event log
             src = outputs if k in outputs else inputs
             setattr(a, k, ptr(src[k]))
         return a
@@ -293,6 +309,13 @@ class ReplayBatch:
         dout = self.alloc_outputs(device=True)
         args = self.args(din, dout, D.ptr)
         D.check(D.lib().strait_replay(C.byref(args), D.stream_handle(stream)))
+        if self.trace:  # an event log that overflowed: re-run with the exact capacity
+            need = int(D.host(dout["counters"]).reshape(self.R, RC_N)[:, RC["TRACE"]].max())
+            if need > self.trace_max:
+                if need > 2**31 - 1:
+                    raise ValueError(f"event log of {need} records exceeds the trace capacity")
+                self.trace_max = need
+                return self.run(stream, metrics, fetch)
         res = {}
         if metrics:
             din["window_ms"] = D.dev(np.array([s.config.goodput_window_ms for s in self.specs], dtype=np.float64))
@@ -303,6 +326,8 @@ class ReplayBatch:
             res.update({"m_" + k: D.host(v) for k, v in mout.items()
                         if fetch is None or k not in series or "m_" + k in fetch})
         res.update({k: D.host(v) for k, v in dout.items() if fetch is None or k in fetch or k == "counters"})
+        if "trace" in res:
+            res["trace"] = res["trace"].view(TRACE_DTYPE)
         res["pred_state"] = D.host(din["pred_state"])
         res["pred_step"] = D.host(din["pred_step"])
         return ReplayResult(self, res)
@@ -374,3 +399,11 @@ class ReplayResult:
         out["pred_step"] = int(self.a["pred_step"][r])
         out["counters"] = self.counters[r]
         return out
+
+    def trace_records(self, r: int) -> np.ndarray:
+        """Replay r's event log (StraitTraceRec, TRACE_DTYPE) in the reference's append order."""
+        if "trace" not in self.a:
+            raise ValueError("replay ran without trace=True")
+        tm = self.batch.trace_max
+        n = int(self.counters[r, RC["TRACE"]])
+        return self.a["trace"][r * tm:r * tm + n]

@@ -440,6 +440,44 @@ def gen_replay(names=None):
                   f"classes {arrays['class_counts'].tolist()}", flush=True)
 
 
+CSV_FILES = ("trace", "requests", "decisions", "feedback", "caps", "batches")
+
+
+def reference_csv_sha(res):
+    """sha256 of each run-directory CSV text the reference writes
+    (report.py:92-106, rows_to_csv_text; trace = SimResult.trace_hash)."""
+    import hashlib
+    from infersim.report import RUN_FILES, rows_to_csv_text
+    payload = {"trace": res.trace_rows, "requests": res.request_rows, "decisions": res.decision_rows,
+               "feedback": res.feedback_rows, "caps": res.cap_rows, "batches": res.batch_rows}
+    out = {k: hashlib.sha256(rows_to_csv_text(payload[k], RUN_FILES[k][1]).encode()).hexdigest() for k in CSV_FILES}
+    assert out["trace"] == res.trace_hash()
+    return out
+
+
+def gen_csvsha(seeds=16):
+    """tests/golden/replay_csv_sha.json: the reference's CSV fingerprints for
+    every golden replay case and for overload.yaml seeds 0..15."""
+    import json
+    import tempfile
+    import yaml
+    import infersim.config as RC
+    from infersim.simulation import Simulation
+    out = {"cases": {}, "overload_seeds": {}}
+    with tempfile.TemporaryDirectory() as tmp:
+        for name in REPLAY_CASES:
+            doc, base = replay_case_docs(name, tmp)
+            out["cases"][name] = reference_csv_sha(Simulation(RC.config_from_dict(doc, base_dir=base)).run())
+            print(" ", name, out["cases"][name]["trace"][:16], flush=True)
+    doc = yaml.safe_load(open("/root/reference/pkg/configs/overload.yaml"))
+    for seed in range(seeds):
+        cfg = RC.config_from_dict(doc, base_dir="/root/reference/pkg/configs")
+        out["overload_seeds"][str(seed)] = reference_csv_sha(Simulation(cfg, seed=seed).run())
+        print("  overload seed", seed, out["overload_seeds"][str(seed)]["trace"][:16], flush=True)
+    with open(os.path.join(HERE, "replay_csv_sha.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1:] or ["predict", "latency", "refit", "sweep", "twa", "replay"]
     if what[0] == "replay" and len(what) > 1:  # gen_golden.py replay <case> ...

@@ -30,8 +30,25 @@ def test_library_exports_every_declared_symbol():
     lib = _abi.lib()
     missing = [n for n in sorted(declared_symbols()) if not hasattr(lib, n)]
     assert not missing, missing
-    assert lib.strait_abi_version() == 1
+    assert lib.strait_abi_version() == _abi.ABI_VERSION
     assert isinstance(lib.strait_last_error(), bytes)
+
+
+def test_ctypes_mirrors_match_the_header_structs():
+    """Every ctypes Structure the host passes through the C-ABI has the size of
+    its C struct (strait_struct_size), so no field is misplaced."""
+    import ctypes as C
+
+    from paper_2604_28175_b200 import _abi, _replay_abi as R, devgen
+
+    lib = _abi.lib()
+    mirrors = [_abi.SweepArgs, _abi.SweepExpandArgs, _abi.RefitArgs, R.ReplayModels, R.ReplayConfig,
+               R.ReplayArgs, None, R.MetricsArgs, devgen.StreamSpec]
+    for i, m in enumerate(mirrors):
+        want = lib.strait_struct_size(i)
+        got = R.TRACE_DTYPE.itemsize if m is None else C.sizeof(m)
+        assert got == want, (i, m, got, want)
+    assert lib.strait_struct_size(99) == -1
 
 
 def test_library_is_sm100a():

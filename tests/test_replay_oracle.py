@@ -58,3 +58,27 @@ def test_replay_batch_many_seeds_parallel(oracle):
     r4 = oracle.replay(b, threads=4)
     for k in ("req_status", "dec_gpu", "dec_est_latency", "counters", "pred_state"):
         np.testing.assert_array_equal(r1.a[k], r4.a[k])
+
+
+def test_csv_fingerprints_are_the_surveys():
+    """The reference CSV fingerprints the GPU byte-identity tests compare against
+    (tests/golden/replay_csv_sha.json) carry the trace hashes SURVEY.md recorded
+    independently: §8(c) for demo / overload / C1, Appendix A for overload seeds 0-15."""
+    import json
+    import re
+
+    from conftest import REPO
+
+    sha = json.load(open(os.path.join(GOLDEN, "replay_csv_sha.json")))
+    survey = open(os.path.join(REPO, "SURVEY.md")).read()
+    app = dict(re.findall(r"^\| (\d+) \| [\d.]+ \| [\d.]+ \| `([0-9a-f]{64})` \|$", survey, flags=re.M))
+    assert len(app) == 16
+    for s, h in app.items():
+        assert sha["overload_seeds"][s]["trace"] == h, s
+    for case, tag in (("demo", "`demo.yaml` seed 1"), ("overload", "`overload.yaml` seed 0"),
+                      ("c1", "C1 restated")):
+        m = re.search(re.escape(tag) + r"[^`]*`([0-9a-f]{64})`", survey)
+        assert m and sha["cases"][case]["trace"] == m.group(1), case
+    assert set(sha["cases"]) == set(CASES)
+    assert all(set(v) == {"trace", "requests", "decisions", "feedback", "caps", "batches"}
+               for v in list(sha["cases"].values()) + list(sha["overload_seeds"].values()))
