@@ -53,7 +53,7 @@ int strait_abi_version(void);
 /* sizeof of each ABI struct, so bindings can verify their mirrors (HOST only):
  * 0 StraitSweepArgs, 1 StraitSweepExpandArgs, 2 StraitRefitArgs, 3 StraitReplayModels,
  * 4 StraitReplayConfig, 5 StraitReplayArgs, 6 StraitTraceRec, 7 StraitMetricsArgs,
- * 8 StraitStreamSpec; -1 for an unknown id */
+ * 8 StraitStreamSpec, 9 StraitGroundTruth; -1 for an unknown id */
 int64_t strait_struct_size(int32_t id);
 const char *strait_last_error(void);
 /* number of device kernels this library launched since load (evidence counter) */
@@ -76,6 +76,22 @@ void strait_host_exp(const double *x, double *y, int64_t n);
  * call, and behind numpy's ziggurat tails).  y may be NULL unless fn == 2.
  */
 int strait_math(int32_t fn, const double *x, const double *y, int64_t n, double *out, void *stream);
+
+/* Hidden ground-truth slowdown of the simulated GPUs (oracle.py:18-77): */
+typedef struct StraitGroundTruth {
+  int32_t family;     /* 0 exponential (scale * base**x + offset), 1 quadratic (scale * x*x + offset) */
+  int32_t n_metrics;  /* == len(weights) */
+  double scale, base, offset, w_cmp, w_mem;
+  double pf_high, pf_low; /* priority_factor */
+  double w[STRAIT_MAX_METRICS];
+} StraitGroundTruth;
+/* out[i] = ground_truth_slowdown(gt, colocated[:, i], self_cmp[i], self_mem[i], prio[i], noise[i])
+ * (oracle.py:55-77): x = w_cmp*cmp + w_mem*mem, then x += w_k*a_k in metric order;
+ * 1 + max(0, effect) * priority_factor * noise.  colocated is [n_metrics][n];
+ * noise is nullable (1.0).  Replaces ground_truth_slowdown (oracle.py:55-77). */
+int strait_gt_slowdown(const StraitGroundTruth *gt, const double *colocated, const double *self_cmp,
+                       const double *self_mem, const int8_t *prio, const double *noise, int64_t n, double *out,
+                       void *stream);
 
 /*
  * R1-R3: batched predict_interference (predictor.py:208-216).

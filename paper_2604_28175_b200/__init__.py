@@ -20,5 +20,9 @@ from .scheduler import (BatchPlan, PredictivePolicy, ScheduleDecision, Schedulin
                         check_violate, complete_batch, early_drop, largest_feasible, make_policy, run_scheduling_pass,
                         submit_plan)
 from .simulation import SimResult, Simulation, run, run_many
+from .config import ExperimentConfig, GroundTruthParams, default_ground_truth, load_config
+from .ground_truth import ground_truth_slowdown
+from .metrics import MetricsReport, compute_metrics, perturb_profiles
+from .workload import WorkloadSpec, gen_poisson, gen_uniform, load_trace
 
 __version__ = "0.1.0"

@@ -159,6 +159,8 @@ def _declare(lib):
     lib.strait_round.argtypes = [C.POINTER(SweepArgs), C.POINTER(RefitArgs), _vp]
     lib.strait_math.restype = C.c_int
     lib.strait_math.argtypes = [C.c_int32, _vp, _vp, C.c_int64, _vp, _vp]
+    lib.strait_gt_slowdown.restype = C.c_int
+    lib.strait_gt_slowdown.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, C.c_int64, _vp, _vp]
     lib.strait_sweep_expand.restype = C.c_int
     lib.strait_sweep_expand.argtypes = [C.POINTER(SweepExpandArgs), C.POINTER(SweepArgs), _vp]
     lib.strait_host_exp.restype = None

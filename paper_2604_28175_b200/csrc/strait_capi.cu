@@ -46,6 +46,7 @@ extern "C" int64_t strait_struct_size(int32_t id) {
     case 6: return sizeof(StraitTraceRec);
     case 7: return sizeof(StraitMetricsArgs);
     case 8: return sizeof(StraitStreamSpec);
+    case 9: return sizeof(StraitGroundTruth);
   }
   return -1;
 }

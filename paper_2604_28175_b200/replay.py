@@ -269,7 +269,13 @@ class ReplayBatch:
                 buf = np.frombuffer(bytes(v), dtype=np.uint8)
                 out[k] = D.dev(buf, torch.uint8)
             else:
-                out[k] = D.dev(v, getattr(torch, np.asarray(v).dtype.name))
+                v = np.asarray(v)
+                if not v.size:  # a replay batch without requests still passes valid (1-element) buffers
+                    v = np.zeros(1, v.dtype)
+                out[k] = D.dev(v, getattr(torch, v.dtype.name))
+        for k, t in out.items():
+            if isinstance(t, torch.Tensor) and not t.numel():
+                out[k] = D.empty(1, t.dtype)
         return out
 
     # ------------------------------------------------------------------ metrics

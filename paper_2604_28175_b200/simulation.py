@@ -27,56 +27,12 @@ from .config import ExperimentConfig
 from .domain import PriorityLevel
 from .predictor import InterferencePredictor
 from ._replay_abi import TR
+from .metrics import ClassMetrics, MetricsReport
 from .replay import ReplayBatch, ReplayResult, ReplaySpec
 
 TRACE_EVENTS = ("arrival", "submit", "drop", "kernel_start", "kernel_complete", "aimd_tick", "aimd_reset")
 
 EV_KERNEL_COMPLETE, EV_TRANSFER_COMPLETE, EV_ARRIVAL, EV_BATCH_TIMEOUT, EV_AIMD_TICK = range(5)
-
-
-@dataclass
-class ClassMetrics:
-    """metrics.py:25-50."""
-
-    arrivals: int = 0
-    completed: int = 0
-    dropped: int = 0
-    violations: int = 0
-    violation_rate_pct: float = 0.0
-    p50_latency: Optional[float] = None
-    p95_latency: Optional[float] = None
-    p99_latency: Optional[float] = None
-    goodput_counts: list = field(default_factory=list)
-
-    def to_dict(self) -> dict:
-        return {"arrivals": self.arrivals, "completed": self.completed, "dropped": self.dropped,
-                "violations": self.violations, "violation_rate_pct": self.violation_rate_pct,
-                "p50_latency_ms": self.p50_latency, "p95_latency_ms": self.p95_latency,
-                "p99_latency_ms": self.p99_latency, "goodput_counts": list(self.goodput_counts)}
-
-
-@dataclass
-class MetricsReport:
-    """metrics.py:53-85, computed on the device (strait_replay_metrics)."""
-
-    per_class: dict
-    window_ms: float
-    intf_error: list
-    latency_error: list
-    kernel_overhead: list
-    cap_timeline: list
-    partial: bool = False
-    _stats: dict = field(default_factory=dict, repr=False)
-
-    def goodput_per_s(self, priority: PriorityLevel) -> list[float]:
-        scale = 1000.0 / self.window_ms
-        return [c * scale for c in self.per_class[priority].goodput_counts]
-
-    def to_dict(self) -> dict:
-        d = {"window_ms": self.window_ms, "partial": self.partial,
-             "high": self.per_class[PriorityLevel.HIGH].to_dict(), "low": self.per_class[PriorityLevel.LOW].to_dict()}
-        d.update(self._stats)
-        return d
 
 
 def _report(res: ReplayResult, r: int) -> MetricsReport:

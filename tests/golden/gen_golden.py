@@ -272,6 +272,35 @@ def gen_twa():
                            for k, v in rows.items()})
 
 
+def gen_gt():
+    """Random (params, co-located aggregate, self terms, priority, noise) ->
+    reference ground_truth_slowdown (oracle.py:55-77), both families,
+    including clamped (effect <= 0) and large-exponent inputs."""
+    from infersim.oracle import GroundTruthParams, ground_truth_slowdown
+    rng = np.random.default_rng(77)
+    rows = {k: [] for k in ("family", "scale", "base", "offset", "w", "w_cmp", "w_mem", "pf", "co", "cmp", "mem",
+                            "prio", "noise", "out")}
+    for i in range(4000):
+        fam = "exponential" if i % 3 else "quadratic"
+        p = GroundTruthParams(family=fam, scale=float(rng.uniform(0.05, 2.0)), base=float(rng.uniform(1.01, 6.0)),
+                              offset=float(rng.uniform(-2.0, 0.5)), weights=tuple(rng.uniform(0, 1, 5).tolist()),
+                              self_compute_weight=float(rng.uniform(0, 1)), self_memory_weight=float(rng.uniform(0, 1)),
+                              priority_factor={PriorityLevel.HIGH: float(rng.uniform(0.2, 1)),
+                                               PriorityLevel.LOW: float(rng.uniform(0.5, 1.5))})
+        co = rng.uniform(0, 3 if i % 7 else 30, 5).tolist()
+        cmp_, mem = float(rng.uniform()), float(rng.uniform())
+        pr = PriorityLevel.HIGH if rng.uniform() < 0.5 else PriorityLevel.LOW
+        noise = float(np.exp(rng.normal(0, 0.05))) if i % 4 else 1.0
+        rows["family"].append(fam == "quadratic"); rows["scale"].append(p.scale); rows["base"].append(p.base)
+        rows["offset"].append(p.offset); rows["w"].append(p.weights); rows["w_cmp"].append(p.self_compute_weight)
+        rows["w_mem"].append(p.self_memory_weight)
+        rows["pf"].append((p.priority_factor[PriorityLevel.HIGH], p.priority_factor[PriorityLevel.LOW]))
+        rows["co"].append(co); rows["cmp"].append(cmp_); rows["mem"].append(mem); rows["prio"].append(int(pr))
+        rows["noise"].append(noise)
+        rows["out"].append(ground_truth_slowdown(p, co, cmp_, mem, pr, noise))
+    np.savez_compressed(os.path.join(HERE, "gt.npz"), **{k: np.array(v) for k, v in rows.items()})
+
+
 # ----------------------------------------------------------------------------- replays
 C1_DOC = {"profiles": "default6", "duration_ms": 26316, "seed": 1, "n_gpus": 1, "policy": "predictive",
           "ground_truth": {"noise_sigma": 0.05},

@@ -45,3 +45,29 @@ def test_shipped_yaml_configs_load_to_the_golden_inputs(name, case):
             assert bytes(a[k]) == bytes(b[k])
         else:
             np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/pkg/src"), reason="reference not mounted")
+def test_perturb_profiles_matches_reference():
+    """metrics.perturb_profiles draws and clamps exactly as the reference's
+    (metrics.py:161-195), value for value."""
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        import infersim.metrics as RM
+        import infersim.profiles as RP
+    finally:
+        sys.path.remove("/root/reference/pkg/src")
+    from paper_2604_28175_b200.metrics import perturb_profiles
+    from paper_2604_28175_b200.profiles import default_profiles
+
+    for mag, seed in ((0.0, 0), (10.0, 3), (35.5, 11), (100.0, 2604)):
+        want = RM.perturb_profiles(RP.default_profiles(), mag, seed)
+        got = perturb_profiles(default_profiles(), mag, seed)
+        assert sorted(want) == sorted(got)
+        for mid in want:
+            for f in ("throughput", "self_compute", "self_memory", "total_latency", "kernel_latency",
+                      "transfer_latency"):
+                assert [tuple(r) if isinstance(r, (list, tuple)) else r for r in getattr(got[mid], f)] == \
+                       [tuple(r) if isinstance(r, (list, tuple)) else r for r in getattr(want[mid], f)], (mid, f)
+    with pytest.raises(ValueError):
+        perturb_profiles(default_profiles(), 101.0, 0)
