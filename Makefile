@@ -36,7 +36,17 @@ oracle/build/libstrait_oracle.so: $(OSRC) $(wildcard include/*.h)
 	@mkdir -p oracle/build
 	gcc -O2 -fPIC -shared -ffp-contract=off -fno-fast-math -fopenmp -o $@ $(OSRC) -lm
 
+# diagnostic: the replay engine with per-phase cycle accounting (scripts/replay_profile.py)
+PROF_LIB := build/prof/_strait.so
+PROF_OBJS := $(patsubst $(CDIR)/%.cu,build/prof/%.o,$(CSRC))
+prof: $(PROF_LIB)
+build/prof/%.o: $(CDIR)/%.cu $(COMMON_HDR) $(REPLAY_HDR)
+	@mkdir -p build/prof
+	$(NVCC) $(NVFLAGS) -DSTRAIT_REPLAY_PROFILE=1 -dc -o $@ $<
+$(PROF_LIB): $(PROF_OBJS)
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(PROF_OBJS)
+
 clean:
 	rm -rf build $(LIB) oracle/build
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean prof

@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_strait.so")
+# STRAIT_LIB: an alternative build of the same library (diagnostic builds, e.g. `make prof`)
+LIB_PATH = os.environ.get("STRAIT_LIB") or os.path.join(_HERE, "_strait.so")
 
 ABI_VERSION = 2  # include/strait.h STRAIT_ABI_VERSION
 STRAIT_OK = 0

@@ -101,3 +101,20 @@ extern "C" int strait_replay(const StraitReplayArgs* a, void* stream) {
   }
   return rc;
 }
+
+#if STRAIT_REPLAY_PROFILE
+namespace strait {
+namespace rp {
+__device__ unsigned long long g_replay_prof[RPF_N];
+}  // namespace rp
+}  // namespace strait
+/* diagnostic build only: accumulated engine cycles per phase since the last call (then reset) */
+extern "C" int strait_replay_profile(unsigned long long* out) {
+  using namespace strait::rp;
+  unsigned long long zero[RPF_N] = {};
+  if (cudaMemcpyFromSymbol(out, g_replay_prof, sizeof zero) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_replay_prof, zero, sizeof zero) != cudaSuccess)
+    return strait::set_error(STRAIT_ECUDA, "strait_replay_profile: copy failed");
+  return RPF_N;
+}
+#endif

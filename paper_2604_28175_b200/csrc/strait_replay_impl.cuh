@@ -46,6 +46,25 @@
 namespace strait {
 namespace rp {
 
+// Cycle accounting of the engine's phases (diagnostic build only:
+// -DSTRAIT_REPLAY_PROFILE=1, scripts/replay_profile.py); compiled out otherwise.
+#ifndef STRAIT_REPLAY_PROFILE
+#define STRAIT_REPLAY_PROFILE 0
+#endif
+#if STRAIT_REPLAY_PROFILE
+enum { RPF_SELECT, RPF_ARRIVAL, RPF_RANK, RPF_DROP, RPF_ELIG, RPF_PROPOSE, RPF_SUBMIT, RPF_ICUR, RPF_TIMEOUTS,
+       RPF_TC, RPF_KC_PRE, RPF_KC_UPDATE, RPF_KC_POST, RPF_TICK, RPF_POST, RPF_TOTAL,
+       RPF_N_QUEUES, RPF_N_ELIGIBLE, RPF_N_PROPOSE_WIDE, RPF_N_SUBMIT, RPF_N_ICUR_ALL, RPF_N };
+#define RP_CNT(i) (++prof[i])
+extern __device__ unsigned long long g_replay_prof[RPF_N];
+#define RP_T(v) const long long v = clock64()
+#define RP_ADD(i, v) (prof[i] += clock64() - (v))
+#else
+#define RP_T(v)
+#define RP_ADD(i, v)
+#define RP_CNT(i)
+#endif
+
 // Two math policies.  The latency variant (few replays, one warp each: C2,
 // C4's longest replays bound the launch) inlines everything.  The throughput
 // variant (16 replays per SM) is instruction-cache bound — 16 warps at
@@ -84,7 +103,10 @@ __host__ __device__ __forceinline__ size_t al(size_t x) { return (x + 15) & ~(si
 // per-GPU fields are [field][G] so lanes over GPUs touch consecutive words.
 // Slot double fields (SD_*), then four NM-vectors: timeline value, timeline
 // integral, the entry's contribution and aggregate_excluding(entry):
-enum { SD_DL, SD_KS, SD_T0, SD_TL, SD_REM, SD_SLOW, SD_NOISE, SD_LAST, SD_WORK, SD_ICUR, SD_CMP, SD_MEM, SD_TK, SD_VL };
+// SD_X0 / SD_RB / SD_ST: the k-independent parts of a co-runner's projection,
+// refreshed with intf_cur (icur_slot)
+enum { SD_DL, SD_KS, SD_T0, SD_TL, SD_REM, SD_SLOW, SD_NOISE, SD_LAST, SD_WORK, SD_RB, SD_X0, SD_ST, SD_CMP, SD_MEM,
+       SD_TK, SD_VL };
 enum { SI_BID, SI_REQ0, SI_N };
 enum { SB_MODEL, SB_SIZE, SB_PRIO, SB_STARTED, SB_LIVE, SB_TLEN, SB_N };
 enum { GD_TAV, GD_CAP, GD_TICK, GD_AGG };  // then NM aggregates, NM LP aggregates, C pending reservations
@@ -154,6 +176,9 @@ struct Sim {
   int64_t next_arr, resolved;
   int64_t c_batches, c_completed, c_passes, c_cap_rows, c_events, c_hp_viol, c_lp_viol, c_hp_drop, c_lp_drop;
   int64_t c_trace;  // trace records produced (TR)
+#if STRAIT_REPLAY_PROFILE
+  mutable long long prof[RPF_N];
+#endif
 
   // ------------------------------------------------------------ accessors
   __device__ __forceinline__ double& SD(int f, int s) const { return sd[f * S + s]; }
@@ -505,10 +530,22 @@ struct Sim {
   // current params (scheduler.py:150-153): a function of (entry timeline, now,
   // params) only, so it is evaluated once per pass (lane per slot) and
   // re-evaluated for a GPU's entries after a submission stamps their timelines.
+  // Everything of the projection (scheduler.py:150-160) that does not depend on
+  // the candidate is cached with it: x0 = w_cmp*cmp + w_mem*mem (the first
+  // step of pressure_exponent), rb = (1 - progress) * t_kernel and
+  // st = max(now, kernel start); per candidate only intf_new remains.
   __device__ __forceinline__ void icur_slot(int s, double now) const {
     double tw[NM];
     tl_twa(s, now, tw);
-    SD(SD_ICUR, s) = pr.predict(tw, SD(SD_CMP, s), SD(SD_MEM, s), SB(SB_PRIO, s));
+    const double cmp = SD(SD_CMP, s), mem = SD(SD_MEM, s);
+    const double intf_cur = pr.predict(tw, cmp, mem, SB(SB_PRIO, s));
+    const double ks = SD(SD_KS, s), tk = SD(SD_TK, s);
+    const double elapsed = py_max(0.0, now - ks);
+    const double denom = intf_cur * tk;
+    const double progress = denom > 0 ? py_min(1.0, MathT::div(elapsed, denom)) : 1.0;
+    SD(SD_RB, s) = (1.0 - progress) * tk;
+    SD(SD_ST, s) = py_max(now, ks);
+    SD(SD_X0, s) = pr.w_cmp * cmp + pr.w_mem * mem;
   }
   __device__ __forceinline__ void icur_all(double now) const {
     for (int s = lane; s < S; s += 32)
@@ -547,20 +584,19 @@ struct Sim {
       const int s = slot_at(g, p);
       const int ep = SB(SB_PRIO, s);
       if (ep > cprio) continue;
-      double nagg[NM];
-#pragma unroll
-      for (int i = 0; i < NM; ++i) nagg[i] = SD(SD_AEX + i, s) + cd.c[i];  // (agg - e.contrib) + add
-      const double intf_new = pr.predict(nagg, SD(SD_CMP, s), SD(SD_MEM, s), ep);
-      const double intf_cur = SD(SD_ICUR, s);
-      const double ks = SD(SD_KS, s), tk = SD(SD_TK, s);
-      const double elapsed = py_max(0.0, now - ks);
-      const double denom = intf_cur * tk;
-      const double progress = denom > 0 ? py_min(1.0, MathT::div(elapsed, denom)) : 1.0;
-      const double remaining = (1.0 - progress) * tk * intf_new;
-      const double projected = py_max(now, ks) + remaining;
-      if (projected > SD(SD_DL, s)) return true;
+      if (projection(s, cd, ep) > SD(SD_DL, s)) return true;
     }
     return false;
+  }
+  // projected completion of co-runner s if the candidate joins (scheduler.py:150-159):
+  // max(now, ks) + ((1 - progress) * t_kernel) * intf_new
+  __device__ __forceinline__ double projection(int s, const Cand& cd, int ep) const {
+    double x = SD(SD_X0, s);  // pressure_exponent of (agg - e.contrib) + add, self terms first
+#pragma unroll
+    for (int i = 0; i < NM; ++i) x += pr.w[i] * (SD(SD_AEX + i, s) + cd.c[i]);
+    bool sat;
+    const double intf_new = 1.0 + pr.effect(x, sat) * (ep == 0 ? pr.coeff[0] : pr.coeff[1]);
+    return SD(SD_ST, s) + SD(SD_RB, s) * intf_new;
   }
 
   // one (size, GPU) pair of best_for (scheduler.py:263-280): has_slot, violate, meet
@@ -687,6 +723,7 @@ struct Sim {
     // segment width: next power of two >= n_gpus
     const int lw = NG <= 1 ? 0 : 32 - __clz(NG - 1);
     if ((kmax << lw) <= 32) {
+      RP_CNT(RPF_N_PROPOSE_WIDE);
       const int W = 1 << lw;
       const int k = (lane >> lw) + 1, g = lane & (W - 1);
       bool found = false;
@@ -747,6 +784,7 @@ struct Sim {
     const int h = QI(QI_HEAD, m), t = QI(QI_TAIL, m);
     if (h == t) return;
     const double floor_latency = tab_total(m, 1), dl = mdeadline(m);
+    if (!((qf[m] + dl) - now < floor_latency)) return;  // the front stays, hence all stay (prefix)
     int ndrop = 0;
     for (int b = h; b < t; b += 32) {
       const int p = b + lane;
@@ -875,6 +913,7 @@ struct Sim {
     // (priority, front arrival, model_id), as a lane-parallel rank sort.
     // key = priority in the top bit | bit pattern of the (>= 0) front arrival;
     // queues that are not ready get ~0 and sort last.
+    RP_T(t_rank);
     unsigned long long* qk = reinterpret_cast<unsigned long long*>(qd);
     const bool use_prio = cf->use_priority_order;
     for (int m = lane; m < M; m += 32) {
@@ -901,23 +940,39 @@ struct Sim {
       n += __popc(__ballot_sync(kFull, rdy));
     }
     sync();
+    RP_ADD(RPF_RANK, t_rank);
     bool icur_ready = false;
     for (int i = 0; i < n && !err; ++i) {
       const int m = QI(QI_ORD, i);
+      RP_T(t_drop);
+      RP_CNT(RPF_N_QUEUES);
       early_drop(m, now);
+      RP_ADD(RPF_DROP, t_drop);
+      RP_T(t_elig);
       const int len = q_len(m);
       if (!len) continue;
       if (!(len >= mmaxb(m) || now >= front_arrival(m) + mtimeout(m))) continue;  // TaskQueue.eligible
+      RP_CNT(RPF_N_ELIGIBLE);
       if (predictive && !icur_ready) {
+        RP_CNT(RPF_N_ICUR_ALL);
         icur_all(now);
         icur_ready = true;
       }
+      RP_ADD(RPF_ELIG, t_elig);
+      RP_T(t_prop);
       Plan plan;
       const int k = predictive ? propose(m, now, plan) : propose_baseline(m, now, plan);
+      RP_ADD(RPF_PROPOSE, t_prop);
       if (!k) continue;
+      RP_T(t_sub);
+      RP_CNT(RPF_N_SUBMIT);
       submit(m, k, plan, now, pass_id);
+      RP_ADD(RPF_SUBMIT, t_sub);
+      RP_T(t_icur);
       if (predictive) icur_gpu(plan.gpu, now);
+      RP_ADD(RPF_ICUR, t_icur);
     }
+    RP_T(t_to);
     // _ensure_timeout for every queue in model order (simulation.py:360-361)
     for (int m0 = 0; m0 < M; m0 += 32) {
       const int m = m0 + lane;
@@ -933,6 +988,7 @@ struct Sim {
       seq += __popc(mask);
     }
     sync();
+    RP_ADD(RPF_TIMEOUTS, t_to);
   }
 
   // ------------------------------------------------------------ event handlers
@@ -1034,7 +1090,9 @@ struct Sim {
     stamp_all(g, now);
     double predicted, residual;
     bool skipped, saturated;
+    RP_T(t_upd);
     update(tw, tab_cmp(m, k), tab_mem(m, k), prio, actual, predicted, residual, skipped, saturated);
+    RP_ADD(RPF_KC_UPDATE, t_upd);
     if (lane == 0) {
       const int64_t o = base + bid;
       A->fb_predicted[o] = predicted;
@@ -1133,7 +1191,12 @@ struct Sim {
     }
     sync();
 
+#if STRAIT_REPLAY_PROFILE
+    for (int i = 0; i < RPF_N; ++i) prof[i] = 0;
+    RP_T(t_all);
+#endif
     while (!err) {
+      RP_T(t_sel);
       // next event: lexicographic argmin of (time, kind << 56 | seq) over all homes
       double bt = INF;
       unsigned long long bk = kNoKey;
@@ -1163,6 +1226,8 @@ struct Sim {
         bi = __shfl_sync(kFull, bi, __ffs(__ballot_sync(kFull, c)) - 1);
       }
       sync();  // the scan's reads of the event homes complete before any handler writes them
+      RP_ADD(RPF_SELECT, t_sel);
+      RP_T(t_h);
       const int kind = (int)(bk >> 56);
       const double now = bt;
       ++c_events;
@@ -1188,11 +1253,14 @@ struct Sim {
         sync();
         pass = q_len(m) == mmaxb(m);
         post_timeout = m;
+        RP_ADD(RPF_ARRIVAL, t_h);
       } else if (kind == kKC) {
         on_kernel_complete(bi, now);
         pass = true;
+        RP_ADD(RPF_KC_PRE, t_h);
       } else if (kind == kTC) {
         on_transfer_complete(bi, now);
+        RP_ADD(RPF_TC, t_h);
       } else if (kind == kTO) {  // _on_timeout (simulation.py:373-376)
         const int m = bi - S;
         const int gen = QI(QI_EGEN, m);
@@ -1206,14 +1274,22 @@ struct Sim {
         trace1(STRAIT_TR_TICK, now);  // simulation.py:468
         pass = true;
         post_tick = true;
+        RP_ADD(RPF_TICK, t_h);
       }
       if (pass && !err) do_pass(now);
+      RP_T(t_post);
       if (post_timeout >= 0) ensure_timeout(post_timeout, now);
       if (post_tick && resolved < N) {
         push_event(S + M, now + cf->aimd_interval, kTICK);
         sync();
       }
+      RP_ADD(RPF_POST, t_post);
     }
+#if STRAIT_REPLAY_PROFILE
+    RP_ADD(RPF_TOTAL, t_all);
+    if (lane == 0)
+      for (int i = 0; i < RPF_N; ++i) atomicAdd(&g_replay_prof[i], (unsigned long long)prof[i]);
+#endif
     if (!err && resolved != N) err = STRAIT_EORDER;  // unresolved requests (simulation.py:491-494)
     sync();
     double* so = A->pred_state + r * 3 * np;
