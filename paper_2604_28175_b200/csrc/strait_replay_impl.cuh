@@ -54,7 +54,8 @@ namespace rp {
 #if STRAIT_REPLAY_PROFILE
 enum { RPF_SELECT, RPF_ARRIVAL, RPF_RANK, RPF_DROP, RPF_ELIG, RPF_PROPOSE, RPF_SUBMIT, RPF_ICUR, RPF_TIMEOUTS,
        RPF_TC, RPF_KC_PRE, RPF_KC_UPDATE, RPF_KC_POST, RPF_TICK, RPF_POST, RPF_TOTAL,
-       RPF_N_QUEUES, RPF_N_ELIGIBLE, RPF_N_PROPOSE_WIDE, RPF_N_SUBMIT, RPF_N_ICUR_ALL, RPF_N };
+       RPF_N_QUEUES, RPF_N_ELIGIBLE, RPF_N_PROPOSE_WIDE, RPF_N_SUBMIT, RPF_N_ICUR_ALL, RPF_SUM_KMAX, RPF_N_NOSLOT,
+       RPF_SUM_ENTRIES, RPF_N };
 #define RP_CNT(i) (++prof[i])
 extern __device__ unsigned long long g_replay_prof[RPF_N];
 #define RP_T(v) const long long v = clock64()
@@ -724,6 +725,16 @@ struct Sim {
     const int lw = NG <= 1 ? 0 : 32 - __clz(NG - 1);
     if ((kmax << lw) <= 32) {
       RP_CNT(RPF_N_PROPOSE_WIDE);
+#if STRAIT_REPLAY_PROFILE
+      prof[RPF_SUM_KMAX] += kmax;
+      {
+        bool any = false;
+        int ne = 0;
+        for (int g = 0; g < NG; ++g) any |= GI(GI_NRUN, g) < CONC, ne += GI(GI_NRUN, g);
+        prof[RPF_N_NOSLOT] += !any;
+        prof[RPF_SUM_ENTRIES] += ne;
+      }
+#endif
       const int W = 1 << lw;
       const int k = (lane >> lw) + 1, g = lane & (W - 1);
       bool found = false;
@@ -892,6 +903,12 @@ struct Sim {
     ++c_batches;
   }
 
+  __device__ __forceinline__ bool has_any_slot() const {
+    bool any = false;
+    for (int g0 = 0; g0 < NG; g0 += 32) any |= __any_sync(kFull, g0 + lane < NG && GI(GI_NRUN, g0 + lane) < CONC);
+    return any;
+  }
+
   // _ensure_timeout for one model (simulation.py:231-238)
   __device__ __forceinline__ void ensure_timeout(int m, double now) {
     if (!q_len(m) || QI(QI_TGEN, m) == QI(QI_FGEN, m)) return;
@@ -942,6 +959,10 @@ struct Sim {
     sync();
     RP_ADD(RPF_RANK, t_rank);
     bool icur_ready = false;
+    // No GPU with a free slot => no policy can place anything (has_slot fails for
+    // every pair; the baselines need len(running) < cap <= limit too), so the
+    // pass only drops: proposes and intf_cur are skipped until a slot exists.
+    bool any_slot = has_any_slot();
     for (int i = 0; i < n && !err; ++i) {
       const int m = QI(QI_ORD, i);
       RP_T(t_drop);
@@ -953,6 +974,7 @@ struct Sim {
       if (!len) continue;
       if (!(len >= mmaxb(m) || now >= front_arrival(m) + mtimeout(m))) continue;  // TaskQueue.eligible
       RP_CNT(RPF_N_ELIGIBLE);
+      if (!any_slot) continue;
       if (predictive && !icur_ready) {
         RP_CNT(RPF_N_ICUR_ALL);
         icur_all(now);
@@ -971,6 +993,7 @@ struct Sim {
       RP_T(t_icur);
       if (predictive) icur_gpu(plan.gpu, now);
       RP_ADD(RPF_ICUR, t_icur);
+      any_slot = has_any_slot();
     }
     RP_T(t_to);
     // _ensure_timeout for every queue in model order (simulation.py:360-361)

@@ -29,7 +29,7 @@ def main():
     lib.strait_replay_profile.restype = C.c_int
     for name, cfg in cases:
         b = ReplayBatch([ReplaySpec(cfg)])
-        out = np.zeros(21, np.uint64)
+        out = np.zeros(24, np.uint64)
         lib.strait_replay_profile(out.ctypes.data)  # reset
         res = b.run(metrics=False)
         lib.strait_replay_profile(out.ctypes.data)
@@ -45,6 +45,9 @@ def main():
         p = c[RC['PASSES']]
         print(f"  per pass: queues visited {out[16] / p:.2f}, eligible {out[17] / p:.2f}, wide proposes "
               f"{out[18] / p:.2f}, submits {out[19] / p:.2f}, icur_all {out[20] / p:.2f}")
+        w = max(int(out[18]), 1)
+        print(f"  per wide propose: mean kmax {out[21] / w:.2f}, no GPU with a slot {100 * out[22] / w:.1f}%, "
+              f"running entries {out[23] / w:.2f}")
 
 
 if __name__ == "__main__":
