@@ -77,6 +77,23 @@ void strait_host_exp(const double *x, double *y, int64_t n);
  */
 int strait_math(int32_t fn, const double *x, const double *y, int64_t n, double *out, void *stream);
 
+/* loss_gradient (predictor.py:271-309) of n independent samples under ONE
+ * parameter vector params[n_metrics + 7]: out_grad is [n_metrics + 7][n]
+ * (huber_grad(residual) * d(prediction)/d(theta), the inactive coefficient 0).
+ * out_saturated is nullable. */
+int strait_loss_gradient(const double *params, int32_t n_metrics, double effect_cap, double huber_delta,
+                         const double *twa, const double *self_cmp, const double *self_mem, const int8_t *prio,
+                         const double *actual, int64_t n, double *out_predicted, double *out_residual,
+                         uint8_t *out_saturated, double *out_grad, void *stream);
+/* One adam_step (predictor.py:124-145) over n entries in place, after the
+ * caller advanced opt.step to t: bc1 = 1 - beta1**t, bc2 = 1 - beta2**t.
+ * active is nullable; inactive entries keep value and moments. */
+int strait_adam_step(double *values, double *m, double *v, const double *grads, const uint8_t *active, int32_t n,
+                     double bc1, double bc2, double learning_rate, double beta1, double beta2, double eps,
+                     void *stream);
+/* huber_loss / huber_grad (predictor.py:148-158); either output nullable. */
+int strait_huber(const double *residual, double delta, int64_t n, double *out_loss, double *out_grad, void *stream);
+
 /* Hidden ground-truth slowdown of the simulated GPUs (oracle.py:18-77): */
 typedef struct StraitGroundTruth {
   int32_t family;     /* 0 exponential (scale * base**x + offset), 1 quadratic (scale * x*x + offset) */

@@ -160,6 +160,12 @@ def _declare(lib):
     lib.strait_round.argtypes = [C.POINTER(SweepArgs), C.POINTER(RefitArgs), _vp]
     lib.strait_math.restype = C.c_int
     lib.strait_math.argtypes = [C.c_int32, _vp, _vp, C.c_int64, _vp, _vp]
+    lib.strait_loss_gradient.restype = C.c_int
+    lib.strait_loss_gradient.argtypes = [_vp, C.c_int32, C.c_double, C.c_double] + [_vp] * 5 + [C.c_int64] + [_vp] * 5
+    lib.strait_adam_step.restype = C.c_int
+    lib.strait_adam_step.argtypes = [_vp] * 5 + [C.c_int32] + [C.c_double] * 6 + [_vp]
+    lib.strait_huber.restype = C.c_int
+    lib.strait_huber.argtypes = [_vp, C.c_double, C.c_int64, _vp, _vp, _vp]
     lib.strait_gt_slowdown.restype = C.c_int
     lib.strait_gt_slowdown.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, C.c_int64, _vp, _vp]
     lib.strait_sweep_expand.restype = C.c_int

@@ -273,6 +273,76 @@ def estimate_latency(params: PredictorParams, profile: ModelProfile, size: int, 
     return float(lat[0])
 
 
+# ----------------------------------------------------------------------------- refit building blocks
+
+def huber_batch(residuals, delta: float):
+    """(huber_loss[n], huber_grad[n]) on the device (predictor.py:148-158)."""
+    r = np.atleast_1d(np.asarray(residuals, dtype=np.float64))
+    dr, loss, grad = D.dev(r), D.empty(max(len(r), 1)), D.empty(max(len(r), 1))
+    D.check(D.lib().strait_huber(D.ptr(dr), float(delta), len(r), D.ptr(loss), D.ptr(grad), D.stream_handle()))
+    return D.host(loss)[:len(r)], D.host(grad)[:len(r)]
+
+
+def huber_loss(residual: float, delta: float) -> float:
+    """predictor.py:148-152."""
+    return float(huber_batch([residual], delta)[0][0])
+
+
+def huber_grad(residual: float, delta: float) -> float:
+    """predictor.py:155-158."""
+    return float(huber_batch([residual], delta)[1][0])
+
+
+def loss_gradient_batch(params: PredictorParams, samples: Sequence["FeedbackSample"], delta: float):
+    """loss_gradient of many samples under one parameter vector, one launch:
+    (predicted[n], residual[n], saturated[n], grads[n][n_params])."""
+    nm = len(params.weights)
+    n = len(samples)
+    tw = np.empty((nm, max(n, 1)))
+    for i, s in enumerate(samples):
+        if len(s.colocated_twa) != nm:
+            raise ValueError(f"aggregate throughput has {len(s.colocated_twa)} metrics, model expects {nm}")
+        tw[:, i] = s.colocated_twa
+    col = lambda f, dt=np.float64: np.array([f(s) for s in samples] or [0], dtype=dt)  # noqa: E731
+    ins = [D.dev(tw), D.dev(col(lambda s: s.self_compute)), D.dev(col(lambda s: s.self_memory)),
+           D.dev(col(lambda s: int(s.priority), np.int8), torch.int8), D.dev(col(lambda s: s.actual))]
+    m = max(n, 1)
+    pred, res, sat, grad = D.empty(m), D.empty(m), D.empty(m, torch.uint8), D.empty(params.n_params() * m)
+    P = params.device_vector()
+    D.check(D.lib().strait_loss_gradient(D.ptr(P), nm, float(params.effect_cap), float(delta),
+                                         *[D.ptr(t) for t in ins], n, D.ptr(pred), D.ptr(res), D.ptr(sat),
+                                         D.ptr(grad), D.stream_handle()))
+    g = D.host(grad).reshape(params.n_params(), m)[:, :n].T
+    return D.host(pred)[:n], D.host(res)[:n], D.host(sat)[:n].astype(bool), g
+
+
+def loss_gradient(params: PredictorParams, sample: "FeedbackSample", delta: float):
+    """predictor.py:303-309: (predicted, residual, saturated, dLoss/dtheta)."""
+    p, r, s, g = loss_gradient_batch(params, [sample], delta)
+    return float(p[0]), float(r[0]), bool(s[0]), [float(x) for x in g[0]]
+
+
+def adam_step(opt: OptimizerState, values: list, grads: Sequence[float],
+              active: Optional[Sequence[bool]] = None) -> None:
+    """predictor.py:124-145: one Adam update in place on the device; inactive
+    entries keep value and moments, the shared step counter advances once.
+    The bias corrections 1 - beta**t are the reference's Python float powers."""
+    opt.step += 1
+    t = opt.step
+    bc1, bc2 = 1.0 - opt.beta1 ** t, 1.0 - opt.beta2 ** t
+    n = len(grads)
+    if n == 0:
+        return
+    dv, dm, dvv = (D.dev(np.asarray(x[:n], dtype=np.float64)) for x in (values, opt.m, opt.v))
+    dg = D.dev(np.asarray(grads, dtype=np.float64))
+    da = D.dev(np.asarray(active, dtype=np.uint8), torch.uint8) if active is not None else None
+    D.check(D.lib().strait_adam_step(D.ptr(dv), D.ptr(dm), D.ptr(dvv), D.ptr(dg), D.ptr(da), n, bc1, bc2,
+                                     opt.learning_rate, opt.beta1, opt.beta2, opt.eps, D.stream_handle()))
+    values[:n] = D.host(dv).tolist()
+    opt.m[:n] = D.host(dm).tolist()
+    opt.v[:n] = D.host(dvv).tolist()
+
+
 # ----------------------------------------------------------------------------- the predictor
 
 class InterferencePredictor:

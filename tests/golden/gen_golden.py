@@ -272,6 +272,42 @@ def gen_twa():
                            for k, v in rows.items()})
 
 
+def gen_lossgrad():
+    """Reference loss_gradient on random (params, sample) pairs, including
+    clamped and saturated ones, plus a 300-step adam_step trajectory with an
+    inactive entry (predictor.py:124-145,271-309)."""
+    from infersim.predictor import FeedbackSample, OptimizerState, PredictorParams, adam_step, loss_gradient
+    rng = np.random.default_rng(303)
+    rows = {k: [] for k in ("P", "twa", "cmp", "mem", "prio", "actual", "pred", "res", "sat", "grad")}
+    for i in range(3000):
+        p = PredictorParams(scale=float(rng.uniform(0.01, 2.0)), base=float(rng.uniform(1.01, 6.0)),
+                            offset=float(rng.uniform(-3.0, 1.0)), weights=tuple(rng.uniform(-0.5, 1.5, 5).tolist()),
+                            self_compute_weight=float(rng.uniform(-0.5, 1.0)),
+                            self_memory_weight=float(rng.uniform(-0.5, 1.0)),
+                            priority_coeff={PriorityLevel.HIGH: float(rng.uniform(0.1, 2.0)),
+                                            PriorityLevel.LOW: float(rng.uniform(0.1, 2.0))})
+        tw = tuple(rng.uniform(0, 3 if i % 5 else 40, 5).tolist())
+        s = FeedbackSample("b", tw, float(rng.uniform()), float(rng.uniform()),
+                           PriorityLevel(int(rng.integers(0, 2))), float(rng.uniform(0.5, 8.0)))
+        pred, res, sat, grad = loss_gradient(p, s, 0.5)
+        rows["P"].append(p.to_vector()); rows["twa"].append(tw); rows["cmp"].append(s.self_compute)
+        rows["mem"].append(s.self_memory); rows["prio"].append(int(s.priority)); rows["actual"].append(s.actual)
+        rows["pred"].append(pred); rows["res"].append(res); rows["sat"].append(sat); rows["grad"].append(grad)
+    out = {k: np.array(v) for k, v in rows.items()}
+    n = 12
+    opt = OptimizerState(m=[0.0] * n, v=[0.0] * n)
+    values = rng.normal(0, 1, n).tolist()
+    out["adam_init"] = np.array(values)
+    grads = rng.normal(0, 2, (300, n))
+    active = [i != 7 for i in range(n)]
+    traj = []
+    for g in grads:
+        adam_step(opt, values, g.tolist(), active=active)
+        traj.append(list(values) + list(opt.m) + list(opt.v))
+    out["adam_grads"], out["adam_traj"], out["adam_active"] = grads, np.array(traj), np.array(active)
+    np.savez_compressed(os.path.join(HERE, "lossgrad.npz"), **out)
+
+
 def gen_gt():
     """Random (params, co-located aggregate, self terms, priority, noise) ->
     reference ground_truth_slowdown (oracle.py:55-77), both families,
