@@ -27,6 +27,26 @@ def test_reference_suite_against_mirror(module, tmp_path):
     assert " passed" in r.stdout and "failed" not in r.stdout
 
 
+# The rest of the reference's scheduler / baseline suites: every test whose
+# functions run on the host mirror (early_drop, TaskQueue, AIMD, the runtime
+# state, largest_feasible, the baseline policies, the pass driver).  The tests
+# that need the device (check_violate / check_meet / PredictivePolicy.propose)
+# are restated in tests/test_scheduler_gpu.py.
+DEVICE_ONLY = "not TestCheckViolate and not TestCheckMeet and not TestSchedulePass and " \
+              "not test_same_early_drop_sets_across_policies"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_TESTS), reason="reference tests not mounted")
+@pytest.mark.parametrize("module", ["test_scheduler", "test_baselines"])
+def test_reference_host_suites_against_mirror(module, tmp_path):
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(REPO, "tests", "ref_shim"), REPO, REF_TESTS]))
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(REF_TESTS, f"{module}.py"), "-q",
+                        "-p", "no:cacheprovider", "-k", DEVICE_ONLY], cwd=tmp_path, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout
+
+
 @pytest.mark.skipif(not os.path.isdir("/root/reference/pkg/configs"), reason="reference configs not mounted")
 @pytest.mark.parametrize("name,case", [("demo.yaml", "demo"), ("overload.yaml", "overload")])
 def test_shipped_yaml_configs_load_to_the_golden_inputs(name, case):

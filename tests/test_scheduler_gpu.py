@@ -307,3 +307,28 @@ def test_simulation_injected_predictor_refit_in_place(cuda):
     np_ = 12
     np.testing.assert_allclose(pred.params.to_vector(), g["pred_state"][:np_], rtol=1e-5)
     assert pred.opt.step == int(g["pred_step"])
+
+
+def test_same_early_drop_sets_across_policies(cuda):
+    """test_baselines.py:139-155: every policy (the predictive one's propose on
+    the device) drops exactly the requests that cannot meet their deadline in
+    isolation, given identical queue state."""
+    from paper_2604_28175_b200.predictor import InterferencePredictor, PredictorParams
+    from paper_2604_28175_b200.scheduler import ScheduleDecision, make_policy, run_scheduling_pass, submit_plan
+
+    def build():
+        return fill_queue(mk_profile("q", deadline_ms=10.0, base_total=3.0, batch_timeout_ms=0.0),
+                          [0.0, 6.0, 7.0, 7.5])
+
+    now = 8.0
+    predictor = InterferencePredictor(PredictorParams(weights=(0.1,)))
+    for name in ("predictive", "temporal", "static", "reactive"):
+        policy = make_policy(name, predictor)
+        q, gpus, dropped = build(), [mk_gpu(0)], []
+
+        def on_submit(queue, plan):
+            submit_plan(queue, plan, gpus, now, "b0")
+            return ScheduleDecision(now, 0, queue.model_id, plan.size, plan.gpu_id, plan.est_latency, plan.intf_pred)
+
+        run_scheduling_pass(policy, [q], gpus, now, on_submit, lambda queue, reqs: dropped.extend(reqs))
+        assert [r.arrival_time for r in dropped] == [0.0], name
