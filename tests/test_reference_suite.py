@@ -37,11 +37,12 @@ DEVICE_ONLY = "not TestCheckViolate and not TestCheckMeet and not TestSchedulePa
 
 
 @pytest.mark.skipif(not os.path.isdir(REF_TESTS), reason="reference tests not mounted")
-@pytest.mark.parametrize("module", ["test_scheduler", "test_baselines"])
-def test_reference_host_suites_against_mirror(module, tmp_path):
+@pytest.mark.parametrize("module,select", [("test_scheduler", DEVICE_ONLY), ("test_baselines", DEVICE_ONLY),
+                                           ("test_metrics", "TestNearestRank or TestPerturbProfiles")])
+def test_reference_host_suites_against_mirror(module, select, tmp_path):
     env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(REPO, "tests", "ref_shim"), REPO, REF_TESTS]))
     r = subprocess.run([sys.executable, "-m", "pytest", os.path.join(REF_TESTS, f"{module}.py"), "-q",
-                        "-p", "no:cacheprovider", "-k", DEVICE_ONLY], cwd=tmp_path, env=env, capture_output=True,
+                        "-p", "no:cacheprovider", "-k", select], cwd=tmp_path, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout
