@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
     const int cprio = active ? ((const int8_t*)(stage + L.cprio))[4 * sl + (int)((tile * spb + sl) & 3)] : 0;
     const int eprio = active ? ((const int8_t*)(stage + L.eprio))[local] : 0;
     bool viol = false;
-    if (active && c < nrun && eprio <= cprio) {
+    if (active && c < nrun && eprio <= cprio && !(diag & 8)) {  // diag 8: skip the projections (timing only)
       double tw[NM], nagg[NM];
 #pragma unroll
       for (int m = 0; m < NM; ++m) tw[m] = ent[(NM + m) * TT + local];
@@ -579,7 +579,8 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
           double assumed[NM];  // check_meet: half the GPU aggregate (scheduler.py:178)
 #pragma unroll
           for (int m = 0; m < NM; ++m) assumed[m] = 0.5 * pair[m * TP + pp];
-          intf = pr.predict(assumed, cand[(NM + 0) * spb + psl], cand[(NM + 1) * spb + psl], pprio);
+          intf = (diag & 16) ? assumed[0]  // diag 16: skip check_meet's prediction (timing only)
+                             : pr.predict(assumed, cand[(NM + 0) * spb + psl], cand[(NM + 1) * spb + psl], pprio);
           const double wait = py_max(0.0, pair[(2 * NM + 1) * TP + pp] - now);  // pcie.py:21-23
           lat = cand[(NM + 2) * spb + psl] + wait + (intf - 1.0) * cand[(NM + 3) * spb + psl] +
                 (now - cand[(NM + 4) * spb + psl]);
