@@ -221,8 +221,8 @@ class ReplayBatch:
         sizes = {"req": max(self.N, 1), "cap": self.R * self.cap_rows_max, "replay": self.R * RC_N}
         out = {}
         for k, (dt, per) in OUTPUTS.items():
-            if device:
-                out[k] = D.empty(sizes[per], getattr(torch, np.dtype(dt).name))
+            if device:  # zeroed: rows past a replay's batch count are never written
+                out[k] = D.empty(sizes[per], getattr(torch, np.dtype(dt).name)).zero_()
             else:
                 out[k] = np.zeros(sizes[per], dtype=dt)
         if self.trace:

@@ -55,8 +55,10 @@ def test_acceptance_c09_c10_c12_c13_on_device(cuda, oracle):
     assert full_hp > 0 and abl_hp >= 2.0 * full_hp, f"c10: {full_hp} -> {abl_hp}"
     # c12: a second launch on the same inputs is identical
     res2 = batch.run()
-    for k in ("req_status", "req_violated", "req_completion", "dec_gpu", "dec_est_latency", "counters"):
-        assert np.array_equal(res.a[k], res2.a[k], equal_nan=True), k
+    for r in range(batch.R):
+        a, b = res.replay_slice(r), res2.replay_slice(r)
+        for k in ("req_status", "req_violated", "req_completion", "dec_gpu", "dec_est_latency", "counters"):
+            assert np.array_equal(a[k], b[k], equal_nan=True), (r, k)
     # c13: consumed isolated work equals each batch's isolated kernel latency
     tab = batch.tab
     nb = 0
