@@ -25,6 +25,9 @@ def main():
     cases = [("overload", MC.config_from_dict(overload_doc(dur)))]
     if len(sys.argv) > 2:
         cases.append((f"c4 lambda={sys.argv[2]} f=0.5", c4_point(float(sys.argv[2]), 0.5, dur)))
+    if len(sys.argv) > 3:
+        from paper_2604_28175_b200.configs import c5
+        cases.append((f"c5 {sys.argv[3]} ms (64 GPUs, 20 models)", c5(float(sys.argv[3]))))
     lib = D.lib()
     lib.strait_replay_profile.restype = C.c_int
     for name, cfg in cases:
