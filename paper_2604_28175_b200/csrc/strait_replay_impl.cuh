@@ -116,7 +116,7 @@ enum { QI_HEAD, QI_TAIL, QI_FGEN, QI_TGEN, QI_EGEN, QI_ORD, QI_N };
 
 struct Layout {
   int G, C, M, NM, S, NE;
-  size_t P, sd, gd, ed, ek, qd, qf, si, gi, qi, sb, go, qb, bytes;
+  size_t P, sd, gd, ed, ek, qd, qf, sl, si, gi, qi, sb, go, qb, bytes;
   __host__ __device__ static int sd_fields(int nm) { return SD_VL + 4 * nm; }
   __host__ __device__ static int gd_fields(int nm, int c) { return GD_AGG + 2 * nm + c; }
   __host__ __device__ Layout(int g, int c, int m, int nm) : G(g), C(c), M(m), NM(nm) {
@@ -135,6 +135,7 @@ struct Layout {
     ek = take(8 * (size_t)NE);
     qd = take(8 * (size_t)M);
     qf = take(8 * (size_t)M);
+    sl = take(4 * (size_t)S);  // scratch slot list (icur_all)
     si = take(4 * (size_t)SI_N * S);
     gi = take(4 * (size_t)GI_N * G);
     qi = take(4 * (size_t)QI_N * M);
@@ -163,6 +164,7 @@ struct Sim {
   // ---- shared-memory state: grouped field arrays of this warp's slice
   double *P, *sd, *gd, *ed, *qd;
   double* qf;  // front arrival time of each non-empty queue (cache of arr(model_req[head]))
+  int* slist;  // scratch list of slots
   unsigned long long* ek;
   int *si, *gi, *qi;
   int8_t *sb, *go, *qb;
@@ -548,9 +550,20 @@ struct Sim {
     SD(SD_ST, s) = py_max(now, ks);
     SD(SD_X0, s) = pr.w_cmp * cmp + pr.w_mem * mem;
   }
+  // intf_cur is read only by check_violate of GPUs that have a free slot
+  // (has_slot is tested first), so only their entries are evaluated: the
+  // slots are compacted into a list and processed 32 at a time
   __device__ __forceinline__ void icur_all(double now) const {
-    for (int s = lane; s < S; s += 32)
-      if (SB(SB_LIVE, s)) icur_slot(s, now);
+    int count = 0;
+    for (int s0 = 0; s0 < S; s0 += 32) {
+      const int s = s0 + lane;
+      const bool need = s < S && SB(SB_LIVE, s) && GI(GI_NRUN, s % G) < CONC;
+      const unsigned m = __ballot_sync(kFull, need);
+      if (need) slist[count + __popc(m & ((1u << lane) - 1))] = s;
+      count += __popc(m);
+    }
+    __syncwarp();
+    for (int i = lane; i < count; i += 32) icur_slot(slist[i], now);
     __syncwarp();
   }
   __device__ __forceinline__ void icur_gpu(int g, double now) const {
@@ -1377,6 +1390,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   S.ek = (unsigned long long*)(base + L.ek);
   S.qd = (double*)(base + L.qd);
   S.qf = (double*)(base + L.qf);
+  S.slist = (int*)(base + L.sl);
   S.si = (int*)(base + L.si);
   S.gi = (int*)(base + L.gi);
   S.qi = (int*)(base + L.qi);
