@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--segments", type=int, default=1 << 16)
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replay-steps", type=int, default=3, help="timed launches of the C4 replay sweep")
@@ -332,7 +332,7 @@ def run_ours(args):
 
     soa_h = c3_round(rank, n_segments=args.segments)
     n_rounds = args.warmup + args.steps
-    fbs = [c3_feedback(rank * 100000 + r) for r in range(max(n_rounds, args.e2e_steps + 1))]
+    fbs = [c3_feedback(rank * 100000 + r) for r in range(max(n_rounds, args.e2e_steps + 2))]
     soa = soa_h.to_device()
     pred = InterferencePredictor()
     P0 = torch.tensor(pred.params.to_vector(), dtype=torch.float64, device="cuda")
@@ -348,7 +348,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     np_ = pred.params.n_params()
 
-    def one_round(r, cur, nxt, events=None):
+    def one_round(r, cur, nxt, events=None, dsoa=None, dout=None):
         # params of round r = cur[:np]; the refit writes round r+1's state into nxt
         nxt.copy_(cur)
         f = dfb[r % len(dfb)]
@@ -356,7 +356,7 @@ def run_ours(args):
                                     f["actual"], bc=bc)
         if events:
             events[0].record()
-        SW.launch_round(soa, cur[:np_], out, args_r)
+        SW.launch_round(dsoa or soa, cur[:np_], dout or out, args_r)
         if events:
             events[1].record()
 
@@ -394,28 +394,54 @@ def run_ours(args):
     pfields = {k: pin(v) for k, v in comp["fields"].items() if k not in ("ent_row", "cand_row")}
     prows = {k: pin(comp["fields"][k]) for k in ("ent_row", "cand_row")}
     ptables = {k: pin(v) for k, v in comp["tables"].items()}
-    dtables = {k: torch.empty_like(v, device="cuda") for k, v in ptables.items()}
-    drows = {k: torch.empty_like(v, device="cuda") for k, v in prows.items()}
     h2d = sum(t.numel() * t.element_size() for d in (pfields, prows, ptables) for t in d.values())
-    host_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in out.items()}
+    # Steps are pipelined over three streams with double-buffered device snapshots and
+    # outputs. Step i's H2D + expand run on the copy stream while step i-1's round runs on
+    # the compute stream and step i-2's decisions go back on the D2H stream. Every step's
+    # copies lie inside the timed region, and the step time is total / steps.
+    soa2 = soa_h.to_device()
+    bufs = [soa, soa2]
+    dtables = [{k: torch.empty_like(v, device="cuda") for k, v in ptables.items()} for _ in range(2)]
+    drows = [{k: torch.empty_like(v, device="cuda") for k, v in prows.items()} for _ in range(2)]
+    outs = [out, SW.alloc_outputs(soa)]
+    host_outs = [{k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in out.items()} for _ in range(2)]
+    host_out = host_outs[0]
     d2h = sum(t.numel() * t.element_size() for t in host_out.values())
-    e2e_ms = []
-    for i in range(args.e2e_steps + 1):
+    s_h2d, s_d2h, s_cmp = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.current_stream()
+
+    def e2e_pipeline(n, first_round):
+        nonlocal cur, nxt
+        ev = {k: [torch.cuda.Event() for _ in range(n)] for k in ("h2d", "cmp", "d2h")}
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
-        for k, t in ptables.items():
-            dtables[k].copy_(t, non_blocking=True)
-        SW.load_compact(soa, pfields, prows, drows, dtables, comp["table_stride"])
-        one_round(i, cur, nxt)
-        cur, nxt = nxt, cur
-        for k, t in out.items():
-            host_out[k].copy_(t, non_blocking=True)
-        ev1.record()
+        t0.record(s_h2d)
+        for i in range(n):
+            b = i % 2
+            with torch.cuda.stream(s_h2d):
+                if i >= 2:
+                    s_h2d.wait_event(ev["cmp"][i - 2])  # snapshot b is free once round i-2 finished
+                for k, t in ptables.items():
+                    dtables[b][k].copy_(t, non_blocking=True)
+                SW.load_compact(bufs[b], pfields, prows, drows[b], dtables[b], comp["table_stride"], stream=s_h2d)
+                ev["h2d"][i].record(s_h2d)
+            s_cmp.wait_event(ev["h2d"][i])
+            if i >= 2:
+                s_cmp.wait_event(ev["d2h"][i - 2])  # outputs b are free once their D2H finished
+            one_round(first_round + i, cur, nxt, dsoa=bufs[b], dout=outs[b])
+            cur, nxt = nxt, cur
+            ev["cmp"][i].record(s_cmp)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev["cmp"][i])
+                for k, t in outs[b].items():
+                    host_outs[b][k].copy_(t, non_blocking=True)
+                ev["d2h"][i].record(s_d2h)
+        t1.record(s_d2h)
         torch.cuda.synchronize()
-        if i:  # first iteration warms the pinned copies
-            e2e_ms.append(ev0.elapsed_time(ev1))
-    e2e_step_ms = float(np.mean(e2e_ms))
+        return t0.elapsed_time(t1) / n
+
+    e2e_pipeline(2, 0)  # warms the pinned copies and the second snapshot
+    e2e_step_ms = e2e_pipeline(args.e2e_steps, 2)
+    host_out = host_outs[(args.e2e_steps - 1) % 2]  # the last step's decisions
 
     preds = predictions_per_round(soa_h)
     alg_bytes = algorithmic_bytes(soa_h)
@@ -453,7 +479,8 @@ def run_ours(args):
         "e2e": {"value": ws * preds / (e2e_step_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step_ms,
                 "path": "pinned profile-indexed snapshot (int16 profile rows + non-derived fields + profile "
-                        "tables) -> H2D -> strait_sweep_expand -> strait_round (C-ABI) -> D2H decisions"},
+                        "tables) -> H2D -> strait_sweep_expand -> strait_round (C-ABI) -> D2H decisions; "
+                        f"{args.e2e_steps} steps pipelined over copy/compute/D2H streams, total / steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "peak_source": peak_src, "kernel": f"strait_round ({path} sweep path)",
                      "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": kern_ms},
