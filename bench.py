@@ -332,7 +332,8 @@ def run_ours(args):
 
     soa_h = c3_round(rank, n_segments=args.segments)
     n_rounds = args.warmup + args.steps
-    fbs = [c3_feedback(rank * 100000 + r) for r in range(max(n_rounds, args.e2e_steps + 2))]
+    # feedback streams of up to 256 distinct rounds, cycled (each round refits on its own 64 samples)
+    fbs = [c3_feedback(rank * 100000 + r) for r in range(min(max(n_rounds, args.e2e_steps + 2), 256))]
     soa = soa_h.to_device()
     pred = InterferencePredictor()
     P0 = torch.tensor(pred.params.to_vector(), dtype=torch.float64, device="cuda")
