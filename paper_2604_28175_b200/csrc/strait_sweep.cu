@@ -552,12 +552,24 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
     for (int o = C / 2; o > 0; o >>= 1) vbits |= __shfl_xor_sync(0xffffffffu, vbits, o, C);
     uint8_t* s_viol = (uint8_t*)(stage + W.res_viol);
     if (active && c == 0) s_viol[pl] = vbits != 0;
-    // all of the tile's projections are published (named barrier of the group's 8 consumer warps)
-    asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(8 * 32) : "memory");
+    // The tile's projections are published on a named barrier of the group's 8
+    // consumer warps. Only the pair warps wait on it (bar.sync); the others
+    // arrive (bar.arrive), release the stage and go on to their next tile, so the
+    // pair / argmin phases of tile k overlap the projections of tile k+1. There is
+    // one barrier per (group, stage): a stage, and with it its barrier, is reused
+    // only after every warp has released it, so arrivals never mix generations.
+    const int npw = (TP + 31) >> 5;
+    const int bar1 = 1 + group * kMaxStages + st;
+    if (wg >= npw) {
+      asm volatile("bar.arrive %0, %1;" ::"r"(bar1), "r"(8 * 32) : "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      continue;
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(bar1), "r"(8 * 32) : "memory");
 
     // ---- 2. pair: LP cap + check_meet, one lane per pair on the first ceil(TP/32) warps ----
-    const int npw = (TP + 31) >> 5;
-    if (wg < npw) {
+    {
       const int pp = wg * 32 + lane;
       if (pp < TP) {
         const int psl = pp / G;
@@ -597,7 +609,7 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
         s_intf[pp] = intf;
         s_adm[pp] = admitted;
       }
-      if (npw > 1) asm volatile("bar.sync %0, %1;" ::"r"(3 + group), "r"(npw * 32) : "memory");
+      if (npw > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + 2 * kMaxStages + group), "r"(npw * 32) : "memory");
     }
 
     // ---- 3. warp 0: best_for argmin per segment ----
