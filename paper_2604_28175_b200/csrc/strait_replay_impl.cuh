@@ -146,7 +146,7 @@ struct Layout {
   }
 };
 
-template <int NM, typename MathT, bool TR>
+template <int NM, typename MathT, bool TR, bool PO>
 struct Sim {
   static constexpr int NP = NM + 7;
   static constexpr int SD_ACC = SD_VL + NM;   // timeline integral
@@ -225,6 +225,8 @@ struct Sim {
   __device__ __forceinline__ int mmaxb(int m) const { return __ldg(&A->models.max_batch[m]); }
   __device__ __forceinline__ int64_t req_at(int pos) const { return __ldg(&A->model_req[pos]); }
   __device__ __forceinline__ double arr(int64_t gidx) const { return __ldg(&A->arr_time[gidx]); }
+  // PO: a predictive-only batch; the baseline policies compile out
+  __device__ __forceinline__ int policy() const { return PO ? STRAIT_POLICY_PREDICTIVE : cf->policy; }
   __device__ __forceinline__ int q_len(int m) const { return QI(QI_TAIL, m) - QI(QI_HEAD, m); }
   __device__ __forceinline__ double front_arrival(int m) const { return qf[m]; }
 
@@ -432,8 +434,8 @@ struct Sim {
   // reactive allowance for ReactiveSpatialPolicy (baselines.py:131-133), a
   // no-op for the other baselines (scheduler.py:225-226).
   __device__ __forceinline__ void signal_hp(int gpu_id, double now) {
-    if (cf->policy != STRAIT_POLICY_PREDICTIVE) {
-      if (cf->policy == STRAIT_POLICY_REACTIVE) {
+    if (policy() != STRAIT_POLICY_PREDICTIVE) {
+      if (policy() == STRAIT_POLICY_REACTIVE) {
         reactive_catch_up(now);
         lp_allowance = max(cf->reactive_min, lp_allowance - 1);
       }
@@ -674,7 +676,7 @@ struct Sim {
   __device__ __forceinline__ int propose_baseline(int m, double now, Plan& plan) const {
     const double front = front_arrival(m);
     const int kmax = min(q_len(m), mmaxb(m));
-    const int pol = cf->policy;
+    const int pol = policy();
     int gpu = -1, size = kmax;
     if (pol == STRAIT_POLICY_TEMPORAL) {  // first idle GPU; largest size meeting the front deadline
       for (int g0 = 0; g0 < NG && gpu < 0; g0 += 32) {
@@ -937,8 +939,8 @@ struct Sim {
   __device__ __forceinline__ void do_pass(double now) {
     const int pass_id = ++pass_seq;
     ++c_passes;
-    const bool predictive = cf->policy == STRAIT_POLICY_PREDICTIVE;
-    if (cf->policy == STRAIT_POLICY_REACTIVE) reactive_catch_up(now);  // begin_pass (baselines.py:113-114)
+    const bool predictive = policy() == STRAIT_POLICY_PREDICTIVE;
+    if (policy() == STRAIT_POLICY_REACTIVE) reactive_catch_up(now);  // begin_pass (baselines.py:113-114)
     // queue_order (scheduler.py:249-255): stable sort of the ready queues by
     // (priority, front arrival, model_id), as a lane-parallel rank sort.
     // key = priority in the top bit | bit pattern of the (>= 0) front arrival;
@@ -1227,6 +1229,7 @@ struct Sim {
     }
     sync();
 
+    if (PO && cf->policy != STRAIT_POLICY_PREDICTIVE) err = STRAIT_EINVAL;  // args.policies was wrong
 #if STRAIT_REPLAY_PROFILE
     for (int i = 0; i < RPF_N; ++i) prof[i] = 0;
     RP_T(t_all);
@@ -1359,7 +1362,7 @@ struct Sim {
 // MINB = minimum resident CTAs of 4 warps per SM: 1 lets ptxas keep the whole
 // replay state in registers (latency: few replays), 4 caps it at 128 registers
 // for 16 resident replays per SM (throughput: replay sweeps).
-template <int NM, int MINB, bool TR>
+template <int NM, int MINB, bool TR, bool PO>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant__ StraitReplayArgs a, int wpc) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int w = threadIdx.x >> 5;
@@ -1368,7 +1371,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   const int64_t r = a.order ? (int64_t)a.order[slot_w] : slot_w;
   const Layout L(a.max_gpus, a.max_concurrency, a.models.n_models, NM);
   unsigned char* base = smem + (size_t)w * L.bytes;
-  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type, TR> S;
+  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type, TR, PO> S;
   S.A = &a;
   S.cf = a.cfg + r;
   S.lane = threadIdx.x & 31;
@@ -1412,23 +1415,27 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
 template <int NM>
 int launch_replay(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb);
 
-template <int NM, int MINB, bool TR>
+template <int NM, int MINB, bool TR, bool PO>
 int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) {
   const size_t smem = smem_per_warp * wpc;
-  if (cudaFuncSetAttribute(replay_kernel<NM, MINB, TR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  if (cudaFuncSetAttribute(replay_kernel<NM, MINB, TR, PO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return set_error(STRAIT_ECUDA, "strait_replay: cannot reserve %zu B of shared memory", smem);
   const unsigned grid = (unsigned)((a.n_replays + wpc - 1) / wpc);
-  replay_kernel<NM, MINB, TR><<<grid, 32 * wpc, smem, st>>>(a, wpc);
+  replay_kernel<NM, MINB, TR, PO><<<grid, 32 * wpc, smem, st>>>(a, wpc);
   return check_launch("strait_replay");
 }
 
 #define STRAIT_INSTANTIATE_REPLAY(NMV)                                                                            \
   template <>                                                                                                     \
   int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb) { \
-    return minb >= 4   ? launch_replay_occ<NMV, 4, false>(a, st, wpc, smem_per_warp)                            \
-           : minb == 0 ? launch_replay_occ<NMV, 1, true>(a, st, wpc, smem_per_warp)                             \
-                       : launch_replay_occ<NMV, 1, false>(a, st, wpc, smem_per_warp);                           \
+    const bool po = a.policies == (1 << STRAIT_POLICY_PREDICTIVE);                                              \
+    if (minb == 0) return launch_replay_occ<NMV, 1, true, false>(a, st, wpc, smem_per_warp);                     \
+    if (minb >= 4)                                                                                                \
+      return po ? launch_replay_occ<NMV, 4, false, true>(a, st, wpc, smem_per_warp)                              \
+                : launch_replay_occ<NMV, 4, false, false>(a, st, wpc, smem_per_warp);                            \
+    return po ? launch_replay_occ<NMV, 1, false, true>(a, st, wpc, smem_per_warp)                                \
+              : launch_replay_occ<NMV, 1, false, false>(a, st, wpc, smem_per_warp);                              \
   }
 
 }  // namespace rp

@@ -236,6 +236,9 @@ class ReplayBatch:
         a.max_gpus = max(s.config.n_gpus for s in self.specs)
         a.max_concurrency = max(s.config.concurrency_limit for s in self.specs)
         a.trace_max = self.trace_max
+        a.policies = 0
+        for s in self.specs:
+            a.policies |= 1 << POLICY_CODES[s.config.policy]
         t = self.tab
         md = a.models
         md.n_models, md.n_metrics, md.stride = t["M"], t["nm"], t["B"]

@@ -81,3 +81,24 @@ def test_mixed_policies_and_device_inputs(cuda, oracle):
         specs.append(ReplaySpec(overload(400.0, policy=p), i))
         specs.append(ReplaySpec(overload(300.0, policy=p, n_gpus=3, concurrency_limit=2), 10 + i))
     _check(specs, oracle, generate="device")
+
+
+def test_predictive_only_kernel_rejects_a_wrong_policy_mask(cuda):
+    """args.policies selects the kernel without the baseline policies; a
+    replay whose policy contradicts the mask fails with ValueError instead of
+    running the wrong policy."""
+    import ctypes as C
+
+    from paper_2604_28175_b200 import _device as D
+    from paper_2604_28175_b200.replay import ReplayBatch, ReplayResult, ReplaySpec
+    from paper_2604_28175_b200.configs import overload
+
+    batch = ReplayBatch([ReplaySpec(overload(200.0, policy="static"))])
+    din, dout = batch.device_inputs(), batch.alloc_outputs(device=True)
+    args = batch.args(din, dout, D.ptr)
+    assert args.policies == 1 << 2
+    args.policies = 1  # claims predictive-only
+    D.check(D.lib().strait_replay(C.byref(args), D.stream_handle()))
+    res = ReplayResult(batch, {k: D.host(v) for k, v in dout.items()})
+    with pytest.raises(ValueError):
+        res.check()
