@@ -146,7 +146,7 @@ struct Layout {
   }
 };
 
-template <int NM, typename MathT, bool TR, bool PO>
+template <int NM, typename MathT, bool TR, bool LEAN>
 struct Sim {
   static constexpr int NP = NM + 7;
   static constexpr int SD_ACC = SD_VL + NM;   // timeline integral
@@ -225,8 +225,10 @@ struct Sim {
   __device__ __forceinline__ int mmaxb(int m) const { return __ldg(&A->models.max_batch[m]); }
   __device__ __forceinline__ int64_t req_at(int pos) const { return __ldg(&A->model_req[pos]); }
   __device__ __forceinline__ double arr(int64_t gidx) const { return __ldg(&A->arr_time[gidx]); }
-  // PO: a predictive-only batch; the baseline policies compile out
-  __device__ __forceinline__ int policy() const { return PO ? STRAIT_POLICY_PREDICTIVE : cf->policy; }
+  // LEAN: a predictive-only batch whose proposes all fit the all-sizes-at-once
+  // path (max batch x pow2ceil(max GPUs) <= 32): the baseline policies and the
+  // probe-by-probe propose compile out, a smaller kernel for the instruction cache
+  __device__ __forceinline__ int policy() const { return LEAN ? STRAIT_POLICY_PREDICTIVE : cf->policy; }
   __device__ __forceinline__ int q_len(int m) const { return QI(QI_TAIL, m) - QI(QI_HEAD, m); }
   __device__ __forceinline__ double front_arrival(int m) const { return qf[m]; }
 
@@ -730,7 +732,7 @@ struct Sim {
   // probe sequence is replayed on the feasibility bits.  Otherwise sizes are probed one at a
   // time with lanes over GPUs.  Probes never repeat, so the reference's memo
   // reduces to the plan of the last feasible probe.
-  __device__ __forceinline__ int propose(int m, double now, Plan& plan) const {
+  __device__ __forceinline__ int propose(int m, double now, Plan& plan) {
     const double front = front_arrival(m);
     const int kmax = min(q_len(m), mmaxb(m));
     const int cprio = mprio(m);
@@ -788,6 +790,10 @@ struct Sim {
         plan = Plan{true, __shfl_sync(kFull, bg, src), __shfl_sync(kFull, bl, src), __shfl_sync(kFull, bi, src)};
       }
       return bestk;
+    }
+    if constexpr (LEAN) {  // the launcher chose LEAN for a geometry that cannot reach here
+      fail(STRAIT_EINVAL);
+      return 0;
     }
     while (lo <= hi) {
       const int mid = (lo + hi) / 2;
@@ -1229,7 +1235,7 @@ struct Sim {
     }
     sync();
 
-    if (PO && cf->policy != STRAIT_POLICY_PREDICTIVE) err = STRAIT_EINVAL;  // args.policies was wrong
+    if (LEAN && cf->policy != STRAIT_POLICY_PREDICTIVE) err = STRAIT_EINVAL;  // args.policies was wrong
 #if STRAIT_REPLAY_PROFILE
     for (int i = 0; i < RPF_N; ++i) prof[i] = 0;
     RP_T(t_all);
@@ -1362,7 +1368,7 @@ struct Sim {
 // MINB = minimum resident CTAs of 4 warps per SM: 1 lets ptxas keep the whole
 // replay state in registers (latency: few replays), 4 caps it at 128 registers
 // for 16 resident replays per SM (throughput: replay sweeps).
-template <int NM, int MINB, bool TR, bool PO>
+template <int NM, int MINB, bool TR, bool LEAN>
 __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant__ StraitReplayArgs a, int wpc) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int w = threadIdx.x >> 5;
@@ -1371,7 +1377,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   const int64_t r = a.order ? (int64_t)a.order[slot_w] : slot_w;
   const Layout L(a.max_gpus, a.max_concurrency, a.models.n_models, NM);
   unsigned char* base = smem + (size_t)w * L.bytes;
-  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type, TR, PO> S;
+  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type, TR, LEAN> S;
   S.A = &a;
   S.cf = a.cfg + r;
   S.lane = threadIdx.x & 31;
@@ -1409,27 +1415,35 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   S.run();
 }
 
+// LEAN instantiations: a predictive-only batch (args.policies) whose largest
+// batch size x pow2ceil(max GPUs) fits one warp, so every propose takes the
+// all-sizes-at-once path
+inline bool lean_batch(const StraitReplayArgs& a) {
+  const int g = a.max_gpus, lw = g <= 1 ? 0 : 32 - __builtin_clz((unsigned)(g - 1));
+  return a.policies == (1 << STRAIT_POLICY_PREDICTIVE) && ((int64_t)a.models.stride << lw) <= 32;
+}
+
 // host side: launch one instantiation (explicitly specialised in strait_replay_nm*.cu);
 // minb = 4 selects the 128-register throughput variant, 0 the traced latency variant,
 // else the latency variant
 template <int NM>
 int launch_replay(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb);
 
-template <int NM, int MINB, bool TR, bool PO>
+template <int NM, int MINB, bool TR, bool LEAN>
 int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) {
   const size_t smem = smem_per_warp * wpc;
-  if (cudaFuncSetAttribute(replay_kernel<NM, MINB, TR, PO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  if (cudaFuncSetAttribute(replay_kernel<NM, MINB, TR, LEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return set_error(STRAIT_ECUDA, "strait_replay: cannot reserve %zu B of shared memory", smem);
   const unsigned grid = (unsigned)((a.n_replays + wpc - 1) / wpc);
-  replay_kernel<NM, MINB, TR, PO><<<grid, 32 * wpc, smem, st>>>(a, wpc);
+  replay_kernel<NM, MINB, TR, LEAN><<<grid, 32 * wpc, smem, st>>>(a, wpc);
   return check_launch("strait_replay");
 }
 
 #define STRAIT_INSTANTIATE_REPLAY(NMV)                                                                            \
   template <>                                                                                                     \
   int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb) { \
-    const bool po = a.policies == (1 << STRAIT_POLICY_PREDICTIVE);                                              \
+    const bool po = lean_batch(a);                                                                                \
     if (minb == 0) return launch_replay_occ<NMV, 1, true, false>(a, st, wpc, smem_per_warp);                     \
     if (minb >= 4)                                                                                                \
       return po ? launch_replay_occ<NMV, 4, false, true>(a, st, wpc, smem_per_warp)                              \
