@@ -108,7 +108,7 @@ __host__ __device__ __forceinline__ size_t al(size_t x) { return (x + 15) & ~(si
 // refreshed with intf_cur (icur_slot)
 enum { SD_DL, SD_KS, SD_T0, SD_TL, SD_REM, SD_SLOW, SD_NOISE, SD_LAST, SD_WORK, SD_RB, SD_X0, SD_ST, SD_CMP, SD_MEM,
        SD_TK, SD_VL };
-enum { SI_BID, SI_REQ0, SI_N };
+enum { SI_BID, SI_REQ0, SI_GPU, SI_J, SI_N };  // SI_GPU / SI_J: s % G and s / G, precomputed
 enum { SB_MODEL, SB_SIZE, SB_PRIO, SB_STARTED, SB_LIVE, SB_TLEN, SB_N };
 enum { GD_TAV, GD_CAP, GD_TICK, GD_AGG };  // then NM aggregates, NM LP aggregates, C pending reservations
 enum { GI_NRUN, GI_PHEAD, GI_PN, GI_N };
@@ -561,7 +561,7 @@ struct Sim {
     int count = 0;
     for (int s0 = 0; s0 < S; s0 += 32) {
       const int s = s0 + lane;
-      const bool need = s < S && SB(SB_LIVE, s) && GI(GI_NRUN, s % G) < CONC;
+      const bool need = s < S && SB(SB_LIVE, s) && GI(GI_NRUN, SI(SI_GPU, s)) < CONC;
       const unsigned m = __ballot_sync(kFull, need);
       if (need) slist[count + __popc(m & ((1u << lane) - 1))] = s;
       count += __popc(m);
@@ -876,7 +876,8 @@ struct Sim {
       qf[m] = next_front;
       QI(QI_FGEN, m) = QI(QI_FGEN, m) + 1;
       GD(GD_TAV, g) = end;
-      GD(GD_PEND + (GI(GI_PHEAD, g) + GI(GI_PN, g)) % C, g) = end;
+      const int tailp = GI(GI_PHEAD, g) + GI(GI_PN, g);  // < 2C: ring index without a division
+      GD(GD_PEND + (tailp >= C ? tailp - C : tailp), g) = end;
       GI(GI_PN, g) = GI(GI_PN, g) + 1;
       SB(SB_MODEL, s) = (int8_t)m;
       SB(SB_SIZE, s) = (int8_t)k;
@@ -1037,7 +1038,7 @@ struct Sim {
 
   // ------------------------------------------------------------ event handlers
   __device__ __forceinline__ void on_transfer_complete(int s, double now) {  // simulation.py:378-394
-    const int g = s % G;
+    const int g = SI(SI_GPU, s);
     const int pn = GI(GI_PN, g);
     if (pn <= 0) {  // PcieLinkState.calibrate with nothing pending (pcie.py:43-44)
       fail(STRAIT_EINVAL);
@@ -1048,7 +1049,7 @@ struct Sim {
       // calibrate (pcie.py:36-53): FIFO => the oldest reservation is this batch's
       const int ph = GI(GI_PHEAD, g);
       const double predicted = GD(GD_PEND + ph, g);
-      const int nph = (ph + 1) % C, npn = pn - 1;
+      const int nph = ph + 1 == C ? 0 : ph + 1, npn = pn - 1;
       GI(GI_PHEAD, g) = nph;
       GI(GI_PN, g) = npn;
       if (!npn) {
@@ -1058,7 +1059,10 @@ struct Sim {
         if (off != 0.0) {
           GD(GD_TAV, g) = GD(GD_TAV, g) + off;
 #pragma unroll 1
-          for (int i = 0; i < npn; ++i) GD(GD_PEND + (nph + i) % C, g) = GD(GD_PEND + (nph + i) % C, g) + off;
+          for (int i = 0; i < npn; ++i) {
+            const int q = nph + i >= C ? nph + i - C : nph + i;
+            GD(GD_PEND + q, g) = GD(GD_PEND + q, g) + off;
+          }
         }
       }
       SB(SB_STARTED, s) = 1;
@@ -1080,7 +1084,7 @@ struct Sim {
 
   // simulation.py:396-460 (+ complete_batch, scheduler.py:327-352)
   __device__ __forceinline__ void on_kernel_complete(int s, double now) {
-    const int g = s % G;
+    const int g = SI(SI_GPU, s), j = SI(SI_J, s);
     const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s), prio = SB(SB_PRIO, s);
     const int bid = SI(SI_BID, s), req0 = SI(SI_REQ0, s);
     bool ok = true;
@@ -1117,7 +1121,6 @@ struct Sim {
     if (!(actual > 0)) fail(STRAIT_EINVAL);
     // GpuRuntimeState.remove_entry (runtime.py:132-141): shift the running list
     const int n = GI(GI_NRUN, g);
-    const int j = s / G;
     int pos = 0;
     while (pos < n && ORD(pos, g) != j) ++pos;
     if (pos == n) fail(STRAIT_ERUNTIME);
@@ -1200,7 +1203,11 @@ struct Sim {
 #pragma unroll
       for (int i = 0; i < NM; ++i) GD(GD_AGG + i, g) = GD(GD_LPA + i, g) = 0.0;
     }
-    for (int s = lane; s < S; s += 32) SB(SB_LIVE, s) = 0;
+    for (int s = lane; s < S; s += 32) {
+      SB(SB_LIVE, s) = 0;
+      SI(SI_GPU, s) = s % G;
+      SI(SI_J, s) = s / G;
+    }
     for (int i = lane; i < NE; i += 32) {
       ed[i] = INF;
       ek[i] = kNoKey;

@@ -448,9 +448,10 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
       prefetch_tmap(&pair_map);
     }
     int64_t tile = blockIdx.x;
-    for (int64_t k = 0; tile < ntiles; ++k, tile += gridDim.x) {
-      const int st = (int)(k % nstages);
-      const uint32_t use = (uint32_t)(k / nstages);
+    // stage index and ring pass kept incrementally (a 64-bit k % nstages costs ~26 instructions)
+    int st = 0;
+    uint32_t use = 0;
+    for (int64_t k = 0; tile < ntiles; ++k, tile += gridDim.x, st = st + 1 < nstages ? st + 1 : (++use, 0)) {
       unsigned char* stage = smem + st * W.stage_bytes;
       mbar_wait(&empty[st], (use & 1) ^ 1);
       if ((diag & 4) && k >= nstages) {
@@ -507,9 +508,12 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
 
   int64_t tile = blockIdx.x + (int64_t)group * gridDim.x;
-  for (int64_t k = group; tile < ntiles; k += groups, tile += (int64_t)groups * gridDim.x) {
-    const int st = (int)(k % nstages);
-    const uint32_t use = (uint32_t)(k / nstages);
+  // st = k % nstages and use = k / nstages for k = group, group + groups, ...,
+  // kept incrementally (groups <= 2 <= nstages: at most one wrap per step)
+  int st = group % nstages;
+  uint32_t use = (uint32_t)(group / nstages);
+  for (int64_t k = group; tile < ntiles;
+       k += groups, tile += (int64_t)groups * gridDim.x, st = st + groups < nstages ? st + groups : (++use, st + groups - nstages)) {
     unsigned char* stage = smem + st * W.stage_bytes;
     mbar_wait(&full[st], use & 1);
     if (diag & 2) {  // diagnostic: data movement only
