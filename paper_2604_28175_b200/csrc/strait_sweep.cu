@@ -508,12 +508,13 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
   const double nan = __longlong_as_double(0x7ff8000000000000LL);
 
   int64_t tile = blockIdx.x + (int64_t)group * gridDim.x;
+  const int64_t tile_step = (int64_t)groups * gridDim.x;
   // st = k % nstages and use = k / nstages for k = group, group + groups, ...,
   // kept incrementally (groups <= 2 <= nstages: at most one wrap per step)
   int st = group % nstages;
   uint32_t use = (uint32_t)(group / nstages);
-  for (int64_t k = group; tile < ntiles;
-       k += groups, tile += (int64_t)groups * gridDim.x, st = st + groups < nstages ? st + groups : (++use, st + groups - nstages)) {
+  for (; tile < ntiles;
+       tile += tile_step, st = st + groups < nstages ? st + groups : (++use, st + groups - nstages)) {
     unsigned char* stage = smem + st * W.stage_bytes;
     mbar_wait(&full[st], use & 1);
     if (diag & 2) {  // diagnostic: data movement only
