@@ -47,7 +47,7 @@ ARG_ARRAYS = ["cfg", "req_off", "arr_time", "arr_model", "model_req", "mr_off", 
 class ReplayArgs(C.Structure):
     _fields_ = [("n_replays", C.c_int32), ("cap_rows_max", C.c_int32), ("n_bc", C.c_int32),
                 ("max_gpus", C.c_int32), ("max_concurrency", C.c_int32), ("trace_max", C.c_int32),
-                ("policies", C.c_int32), ("pad", C.c_int32),
+                ("policies", C.c_int32), ("uniform", C.c_int32),
                 ("models", ReplayModels)] + [(k, _vp) for k in ARG_ARRAYS]
 
 

@@ -239,6 +239,8 @@ class ReplayBatch:
         a.policies = 0
         for s in self.specs:
             a.policies |= 1 << POLICY_CODES[s.config.policy]
+        a.uniform = int(all(s.config.n_gpus == a.max_gpus and s.config.concurrency_limit == a.max_concurrency
+                            for s in self.specs))
         t = self.tab
         md = a.models
         md.n_models, md.n_metrics, md.stride = t["M"], t["nm"], t["B"]

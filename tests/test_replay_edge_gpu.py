@@ -102,3 +102,25 @@ def test_predictive_only_kernel_rejects_a_wrong_policy_mask(cuda):
     res = ReplayResult(batch, {k: D.host(v) for k, v in dout.items()})
     with pytest.raises(ValueError):
         res.check()
+
+
+def test_fixed_geometry_kernel_rejects_a_wrong_uniform_flag(cuda):
+    """args.uniform + the 4x4x6 geometry select the fixed-geometry kernel; a
+    replay that does not have that geometry fails with ValueError instead of
+    running with the wrong strides."""
+    import ctypes as C
+
+    from paper_2604_28175_b200 import _device as D
+    from paper_2604_28175_b200.configs import overload
+    from paper_2604_28175_b200.replay import ReplayBatch, ReplayResult, ReplaySpec
+
+    batch = ReplayBatch([ReplaySpec(overload(200.0)), ReplaySpec(overload(200.0, n_gpus=2))])
+    din, dout = batch.device_inputs(), batch.alloc_outputs(device=True)
+    args = batch.args(din, dout, D.ptr)
+    assert args.uniform == 0
+    args.uniform = 1  # wrongly claims every replay has 4 GPUs
+    D.check(D.lib().strait_replay(C.byref(args), D.stream_handle()))
+    res = ReplayResult(batch, {k: D.host(v) for k, v in dout.items()})
+    assert int(res.counters[0, 0]) == 0 and int(res.counters[1, 0]) != 0
+    with pytest.raises(ValueError):
+        res.check()
