@@ -154,17 +154,29 @@ struct Layout {
 // field offset folds into an immediate (a ~20 % smaller, faster kernel).
 template <int GEOM>
 struct Geom {
-  int G, C, M, S, NE, NG, CONC;
-  __device__ __forceinline__ bool set_geom(const Layout& L, const StraitReplayConfig* cf) {
-    G = L.G, C = L.C, M = L.M, S = L.S, NE = L.NE, NG = cf->n_gpus, CONC = cf->concurrency_limit;
+  int G, C, M, S, NE, NG, CONC, B;  // B: profile-table stride (max batch size)
+  __device__ __forceinline__ bool set_geom(const Layout& L, const StraitReplayConfig* cf, int stride) {
+    G = L.G, C = L.C, M = L.M, S = L.S, NE = L.NE, NG = cf->n_gpus, CONC = cf->concurrency_limit, B = stride;
     return true;
   }
 };
 template <>
 struct Geom<1> {
   static constexpr int G = 4, C = 4, M = 6, S = 16, NE = 24, NG = 4, CONC = 4;
-  __device__ __forceinline__ bool set_geom(const Layout& L, const StraitReplayConfig* cf) const {
+  int B;
+  __device__ __forceinline__ bool set_geom(const Layout& L, const StraitReplayConfig* cf, int stride) {
+    B = stride;
     return L.G == G && L.C == C && L.M == M && cf->n_gpus == NG && cf->concurrency_limit == CONC;
+  }
+};
+// GEOM 2: GEOM 1 with the table stride (max batch 8) fixed too.  The latency
+// kernel gains (+2-3 %); the 128-register throughput kernel allocates worse
+// with it (-9 %), so that one keeps GEOM 1.
+template <>
+struct Geom<2> {
+  static constexpr int G = 4, C = 4, M = 6, S = 16, NE = 24, NG = 4, CONC = 4, B = 8;
+  __device__ __forceinline__ bool set_geom(const Layout& L, const StraitReplayConfig* cf, int stride) const {
+    return L.G == G && L.C == C && L.M == M && cf->n_gpus == NG && cf->concurrency_limit == CONC && stride == B;
   }
 };
 
@@ -177,6 +189,7 @@ struct Sim : Geom<GEOM> {
   using Geom<GEOM>::NE;
   using Geom<GEOM>::NG;
   using Geom<GEOM>::CONC;
+  using Geom<GEOM>::B;
   static constexpr int NP = NM + 7;
   static constexpr int SD_ACC = SD_VL + NM;   // timeline integral
   static constexpr int SD_CON = SD_VL + 2 * NM;  // entry.contribution (throughput_at(size))
@@ -187,7 +200,6 @@ struct Sim : Geom<GEOM> {
   const StraitReplayArgs* A;
   const StraitReplayConfig* cf;
   int lane;
-  int B;                  // profile-table stride (max batch size)
   int64_t r, base, N;     // request range [base, base + N)
   // ---- shared-memory state: grouped field arrays of this warp's slice
   double *P, *sd, *gd, *ed, *qd;
@@ -822,19 +834,20 @@ struct Sim : Geom<GEOM> {
     if constexpr (LEAN) {  // the launcher chose LEAN for a geometry that cannot reach here
       fail(STRAIT_EINVAL);
       return 0;
-    }
-    while (lo <= hi) {
-      const int mid = (lo + hi) / 2;
-      const Plan p = best_for(m, mid, cprio, dl, front, now);
-      if (p.ok) {
-        bestk = mid;
-        plan = p;
-        lo = mid + 1;
-      } else {
-        hi = mid - 1;
+    } else {
+      while (lo <= hi) {
+        const int mid = (lo + hi) / 2;
+        const Plan p = best_for(m, mid, cprio, dl, front, now);
+        if (p.ok) {
+          bestk = mid;
+          plan = p;
+          lo = mid + 1;
+        } else {
+          hi = mid - 1;
+        }
       }
+      return bestk;
     }
-    return bestk;
   }
 
   // early_drop (scheduler.py:65-75).  deadline_abs - now is monotone in queue
@@ -1417,7 +1430,7 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   S.cf = a.cfg + r;
   S.lane = threadIdx.x & 31;
   S.r = r;
-  if (!S.set_geom(L, S.cf)) {  // the launcher chose a fixed geometry this replay does not have
+  if (!S.set_geom(L, S.cf, a.models.stride)) {  // the launcher chose a fixed geometry this replay does not have
     if (S.lane == 0) {
       int64_t* c = a.counters + r * STRAIT_RC_N;
       for (int i = 0; i < STRAIT_RC_N; ++i) c[i] = 0;
@@ -1425,7 +1438,6 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
     }
     return;
   }
-  S.B = a.models.stride;
   S.base = a.req_off[r];
   S.N = a.req_off[r + 1] - S.base;
   S.P = (double*)(base + L.P);
@@ -1490,7 +1502,8 @@ int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_
     if constexpr (NMV == 5)                                                                                       \
       if (po && overload_geometry(a))                                                                             \
         return minb >= 4 ? launch_replay_occ<NMV, 4, false, true, 1>(a, st, wpc, smem_per_warp)                  \
-                         : launch_replay_occ<NMV, 1, false, true, 1>(a, st, wpc, smem_per_warp);                 \
+                         : a.models.stride == 8 ? launch_replay_occ<NMV, 1, false, true, 2>(a, st, wpc, smem_per_warp) \
+                                                : launch_replay_occ<NMV, 1, false, true, 1>(a, st, wpc, smem_per_warp); \
     if (minb >= 4)                                                                                                \
       return po ? launch_replay_occ<NMV, 4, false, true, 0>(a, st, wpc, smem_per_warp)                           \
                 : launch_replay_occ<NMV, 4, false, false, 0>(a, st, wpc, smem_per_warp);                         \
