@@ -1498,6 +1498,9 @@ int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_
   template <>                                                                                                     \
   int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb) { \
     const bool po = lean_batch(a);                                                                                \
+    if constexpr (NMV == 5) /* traced: run() / Simulation.run() of the overload geometry */                     \
+      if (minb == 0 && po && overload_geometry(a) && a.models.stride == 8)                                       \
+        return launch_replay_occ<NMV, 1, true, true, 2>(a, st, wpc, smem_per_warp);                             \
     if (minb == 0) return launch_replay_occ<NMV, 1, true, false, 0>(a, st, wpc, smem_per_warp);                  \
     if constexpr (NMV == 5)                                                                                       \
       if (po && overload_geometry(a))                                                                             \
