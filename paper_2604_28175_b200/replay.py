@@ -9,6 +9,7 @@ executes every replay to completion in ONE launch of the CUDA engine
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import math
 from dataclasses import dataclass
@@ -313,6 +314,24 @@ class ReplayBatch:
                  "kernel_overhead": (max(self.N, 1), torch.float64)}
         return {k: D.empty(n, dt) for k, (n, dt) in sizes.items()}
 
+    def launch(self, stream=None, metrics: bool = True) -> "PendingReplay":
+        """Enqueue the replay (+ device metrics) without waiting: the host is
+        free to build the next batch while this one runs (`PendingReplay.result`
+        collects it).  Untraced batches only (a trace may need a re-run)."""
+        if self.trace:
+            raise ValueError("launch() is for untraced batches; use run() with trace=True")
+        din = self.device_inputs()
+        dout = self.alloc_outputs(device=True)
+        args = self.args(din, dout, D.ptr)
+        D.check(D.lib().strait_replay(C.byref(args), D.stream_handle(stream)))
+        mout = None
+        if metrics:
+            din["window_ms"] = D.dev(np.array([s.config.goodput_window_ms for s in self.specs], dtype=np.float64))
+            mout = self.alloc_metrics()
+            margs = self.metrics_args(din, dout, mout, D.ptr)
+            D.check(D.lib().strait_replay_metrics(C.byref(margs), D.stream_handle(stream)))
+        return PendingReplay(self, din, dout, mout, stream)
+
     def run(self, stream=None, metrics: bool = True, fetch=None) -> "ReplayResult":
         """Host in, device replay (+ device metrics), host out.  `fetch`
         limits the device->host copy to those output arrays (default: all)."""
@@ -342,6 +361,27 @@ class ReplayBatch:
         res["pred_state"] = D.host(din["pred_state"])
         res["pred_step"] = D.host(din["pred_step"])
         return ReplayResult(self, res)
+
+
+class PendingReplay:
+    """A launched replay batch (ReplayBatch.launch); result() copies it back."""
+
+    def __init__(self, batch, din, dout, mout, stream):
+        self.batch, self.din, self.dout, self.mout, self.stream = batch, din, dout, mout, stream
+
+    def result(self, fetch=None) -> "ReplayResult":
+        ctx = torch.cuda.stream(self.stream) if self.stream is not None else contextlib.nullcontext()
+        with ctx:
+            res = {}
+            if self.mout is not None:
+                series = ("intf_error", "latency_error", "kernel_overhead")
+                res.update({"m_" + k: D.host(v) for k, v in self.mout.items()
+                            if fetch is None or k not in series or "m_" + k in fetch})
+            res.update({k: D.host(v) for k, v in self.dout.items()
+                        if fetch is None or k in fetch or k == "counters"})
+            res["pred_state"] = D.host(self.din["pred_state"])
+            res["pred_step"] = D.host(self.din["pred_step"])
+        return ReplayResult(self.batch, res)
 
 
 class ReplayResult:
