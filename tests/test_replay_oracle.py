@@ -82,3 +82,14 @@ def test_csv_fingerprints_are_the_surveys():
     assert set(sha["cases"]) == set(CASES)
     assert all(set(v) == {"trace", "requests", "decisions", "feedback", "caps", "batches"}
                for v in list(sha["cases"].values()) + list(sha["overload_seeds"].values()))
+
+
+def test_launch_api_is_for_untraced_batches():
+    """ReplayBatch.launch() (asynchronous) rejects traced batches before any
+    device work: a trace may overflow and need a synchronous re-run."""
+    from paper_2604_28175_b200.replay import ReplayBatch, ReplaySpec
+
+    b = ReplayBatch([ReplaySpec(case_config("demo"))], trace=True)
+    with pytest.raises(ValueError, match="untraced"):
+        b.launch()
+    assert b.trace_max > 0 and ReplayBatch([ReplaySpec(case_config("demo"))]).trace_max == 0
