@@ -31,6 +31,12 @@
 //  * Binary64 throughout, --fmad=false, left-to-right evaluation as the
 //    reference, exp/log/pow restated from the reference host's glibc
 //    (strait_libm.cuh): results are bit-identical to the reference.
+//  * Specialised instantiations, because the engine is instruction-cache and
+//    latency bound and every instruction removed pays.  These are MINB
+//    (latency / throughput register budgets), TR (event log compiled in or
+//    out), LEAN (predictive-only batches whose proposes all take the
+//    all-sizes path) and GEOM (the 4 GPU x 4 slot x 6 model geometry as
+//    constants, so every field offset is an immediate).
 #pragma once
 
 #include <cuda_runtime.h>
