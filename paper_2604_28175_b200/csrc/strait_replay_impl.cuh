@@ -186,6 +186,18 @@ struct Geom<2> {
   }
 };
 
+// GEOM 3: the BASELINE C5 geometry (64 GPUs x 4 slots, 20 models), every replay
+// at the maxima.
+template <>
+struct Geom<3> {
+  static constexpr int G = 64, C = 4, M = 20, S = 256, NE = 278, NG = 64, CONC = 4;
+  int B;
+  __device__ __forceinline__ bool set_geom(const Layout& L, const StraitReplayConfig* cf, int stride) {
+    B = stride;
+    return L.G == G && L.C == C && L.M == M && cf->n_gpus == NG && cf->concurrency_limit == CONC;
+  }
+};
+
 template <int NM, typename MathT, bool TR, bool LEAN, int GEOM>
 struct Sim : Geom<GEOM> {
   using Geom<GEOM>::G;
@@ -1483,6 +1495,10 @@ inline bool overload_geometry(const StraitReplayArgs& a) {
   return a.uniform && a.max_gpus == 4 && a.max_concurrency == 4 && a.models.n_models == 6;
 }
 
+inline bool c5_geometry(const StraitReplayArgs& a) {
+  return a.uniform && a.max_gpus == 64 && a.max_concurrency == 4 && a.models.n_models == 20;
+}
+
 // host side: launch one instantiation (explicitly specialised in strait_replay_nm*.cu);
 // minb = 4 selects the 128-register throughput variant, 0 the traced latency variant,
 // else the latency variant
@@ -1508,6 +1524,8 @@ int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_
       if (minb == 0 && po && overload_geometry(a) && a.models.stride == 8)                                       \
         return launch_replay_occ<NMV, 1, true, true, 2>(a, st, wpc, smem_per_warp);                             \
     if (minb == 0) return launch_replay_occ<NMV, 1, true, false, 0>(a, st, wpc, smem_per_warp);                  \
+    if constexpr (NMV == 5)                                                                                       \
+      if (minb == 1 && c5_geometry(a)) return launch_replay_occ<NMV, 1, false, false, 3>(a, st, wpc, smem_per_warp); \
     if constexpr (NMV == 5)                                                                                       \
       if (po && overload_geometry(a))                                                                             \
         return minb >= 4 ? launch_replay_occ<NMV, 4, false, true, 1>(a, st, wpc, smem_per_warp)                  \
