@@ -409,6 +409,9 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
                     int diag, const __grid_constant__ CUtensorMap ent_map,
                     const __grid_constant__ CUtensorMap pair_map, int use_tmap) {
   extern __shared__ __align__(128) unsigned char smem[];
+#if !STRAIT_SWEEP_DIAG_BUILD
+  diag = 0;  // the timing diagnostics (STRAIT_SWEEP_DIAG) exist only in a -DSTRAIT_SWEEP_DIAG_BUILD=1 build
+#endif
   const TileGeom tg(SG ? SG : a.gpus_per_segment, C);
   const WsLayout<NM> W(tg, nstages);
   const StageLayout<NM>& L = W.st;

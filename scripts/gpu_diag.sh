@@ -1,3 +1,4 @@
+# needs a diagnostics build: make clean-free rebuild of strait_sweep.o with -DSTRAIT_SWEEP_DIAG_BUILD=1
 # sweep kernel diagnostics: tensor-map vs bulk, data-movement-only vs full, stages/groups
 nvidia-smi -L
 python -m pytest tests -m gpu -q -p no:cacheprovider -k "sweep or round" > gpurun_out/pytest_gpu.txt 2>&1; tail -3 gpurun_out/pytest_gpu.txt
