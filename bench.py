@@ -256,7 +256,7 @@ def replay_leg(args, ws, rank, local, dist):
         return (time.perf_counter() - t0) * 1e3 / n, res
 
     e2e_pipeline(1)  # warm-up: module load, pinned staging
-    e2e_ms_step, res2 = e2e_pipeline(3)
+    e2e_ms_step, res2 = e2e_pipeline(4)
     e2e = [e2e_ms_step]
     b2 = res2.batch
     h2d = int(sum(np.asarray(v).nbytes for k, v in b2.inputs.items() if k != "cfg") + len(bytes(b2.inputs["cfg"])))
@@ -281,7 +281,7 @@ def replay_leg(args, ws, rank, local, dist):
                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                    "path": "ReplayBatch(specs, generate='device').launch() / .result(): configs + stream specs "
                            "H2D -> device streams -> strait_replay -> device metrics -> D2H outcomes (wall clock); "
-                           "3 steps pipelined (step i+1's batch built on a second stream while step i runs)"},
+                           "4 steps pipelined (step i+1's batch built on a second stream while step i runs)"},
            "host_input_build_s": build_s, "gpu_launches": launches,
            "bound": "latency (one warp per replay); no roofline claim, DESIGN.md 3.3"}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
