@@ -7,18 +7,29 @@ fused with the sequential online refit of F = 64 feedback samples, in one
 launch (strait_round).  Metric: latency predictions/sec (one per projected
 co-runner triple + one check_meet estimate per pair).
 
+The same JSON line carries the other BASELINE configs as legs, each with its
+device time, an end-to-end number through the public API, a CPU baseline
+and a parity verdict against the CPU oracle on exactly the benched inputs:
+  c3_strong  C3 with the round's segments split over the ranks (§8(e))
+  c4         1,024-replay load x HP-fraction sweep (configs[3]), LPT-sharded
+  c1, c2     single replays of 9,858 and ~1M requests (configs[0], [1])
+  c5         the first ~1M requests of the 100M-request 64-GPU replay
+             (configs[4]), with the labelled extrapolation to 100M
+
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1: launched by torchrun, one rank per GPU; every rank sweeps its own
-round of the same shape (weak scaling, no data-path collective); the only
-collective is the end-of-run NCCL all-reduce of the timing / checksum.
+N > 1: launched by torchrun, one rank per GPU.  C3 weak scaling (the
+headline) gives every rank its own round; C3 strong splits one round into
+contiguous slices of whole segments; C4 shards replays longest-first; the
+single-replay configs run one replica per rank.  The only collectives are
+the end-of-run NCCL all-reduces of times and counters.
 --impl reference times the CPU oracle port of the reference path
-(oracle/, all host threads) on a bounded sample of the same workload.
+(oracle/strait_oracle.c, all host threads): the reference is pure Python and
+cannot travel to the GPU box, so the port is its CPU implementation there.
 """
 from __future__ import annotations
 
 import argparse
-import ctypes as C
 import json
 import os
 import sys
@@ -32,6 +43,7 @@ sys.path.insert(0, REPO)
 
 METRIC = "latency predictions/sec (candidate sweep + refit round)"
 UNIT = "predictions/s"
+REPLAY_UNIT = "simulated requests/s"
 
 
 def parse():
@@ -44,9 +56,12 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity checks (timing only)")
     ap.add_argument("--replay-steps", type=int, default=3, help="timed launches of the C4 replay sweep")
     ap.add_argument("--replay-seeds", type=int, default=16, help="seeds per C4 grid point (16 = BASELINE C4)")
-    ap.add_argument("--no-replay", action="store_true")
+    ap.add_argument("--no-replay", action="store_true", help="C3 only")
+    ap.add_argument("--no-single", action="store_true", help="skip the single-replay legs (C1, C2, C5)")
+    ap.add_argument("--c5-full", action="store_true", help="also run the whole 100M-request C5 replay (~20 min)")
     return ap.parse_args()
 
 
@@ -57,15 +72,38 @@ def dist_env():
     return ws, rank, local
 
 
-def predictions_per_round(soa) -> int:
-    return soa.n_triples + soa.n_pairs
+def loaded_repo_libs() -> list[str]:
+    """Shared objects of this repo mapped into the process (evidence of which
+    native code ran: the product's _strait.so, or only the oracle)."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for line in f:
+                p = line.split()[-1] if line.strip() else ""
+                if p.startswith(REPO) and ".so" in os.path.basename(p):
+                    out.add(os.path.relpath(p, REPO))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 def config_block(args, ws):
+    from paper_2604_28175_b200.microbench import C3_CONCURRENCY
+
     return {"workload": "C3 candidate-sweep microbench (BASELINE configs[2])",
             "segments_per_gpu": args.segments, "gpus_per_segment": 64, "slots": 4,
             "triples_per_gpu_round": args.segments * 64 * 4, "refit_samples_per_round": 64,
-            "n_metrics": 5, "parallelism": f"replicated rounds x{ws} (weak)",
+            "n_metrics": 5, "concurrency_limit": C3_CONCURRENCY,
+            "concurrency_note": "limit 5 > 4 slots: every pair has a slot, so every live co-runner is projected "
+                                "(the maximum-work round; the reference default is 4)",
+            "parallelism": f"one round per rank x{ws} (weak); c3_strong splits one round (strong)",
             "l2": "inputs (2.5 GB/round) > 126 MB L2; no flush needed"}
 
 
@@ -121,251 +159,99 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-# ----------------------------------------------------------------------------- reference arm
-def cpu_round_rate(soa, fb, seconds: float, threads: int):
-    """Oracle port: full sweep rounds (+ refit) on `threads` host threads for ~`seconds`."""
+# ----------------------------------------------------------------------------- C3 helpers
+P_INIT = np.array([0.1, np.e, 0.0] + [0.1] * 5 + [0.1, 0.1, 0.5, 1.0])  # PredictorParams() defaults
+
+
+def cpu_rounds(soa, fbs, steps: int, warmup: int, threads: int):
+    """Oracle port: `warmup` + `steps` full sweep rounds with the refit chain
+    (round r refits on fbs[r]) on `threads` host threads; returns the timed
+    rounds' predictions/s and seconds."""
     from oracle import oracle
 
-    P = np.array([0.1, np.e, 0.0] + [0.1] * 5 + [0.1, 0.1, 0.5, 1.0])
-    state = np.concatenate([P, np.zeros(24)])
-    t0 = time.perf_counter()
-    rounds = 0
-    segs = 0
-    chunk = max(256, soa.n_segments // 8)
-    while True:
-        for s0 in range(0, soa.n_segments, chunk):
-            oracle.sweep(soa, state[:12], threads=threads, seg_range=(s0, min(soa.n_segments, s0 + chunk)))
-            segs += min(soa.n_segments, s0 + chunk) - s0
-            if time.perf_counter() - t0 > seconds:
-                break
-        else:
-            state, _, _, _, _ = oracle.refit(state, rounds, fb, nm=5)
-            rounds += 1
-        if time.perf_counter() - t0 > seconds:
-            break
-    dt = time.perf_counter() - t0
-    preds = segs * 64 * 4 + segs * 64
-    return preds / dt, dt, segs
-
-
-# ----------------------------------------------------------------------------- C4 replay sweep
-REPLAY_UNIT = "simulated requests/s"
-
-
-def c4_shard(args, ws, rank):
-    """BASELINE configs[3]: 8 loads x 8 HP fractions x seeds replays of overload's
-    3 s horizon; replay r runs on rank r mod N (strong scaling)."""
-    from paper_2604_28175_b200.configs import c4_grid
-    from paper_2604_28175_b200.replay import ReplaySpec
-    from paper_2604_28175_b200.shard import shard
-
-    grid = c4_grid(seeds=args.replay_seeds)
-    return [ReplaySpec(c, s) for c, s in shard(grid, ws, rank)], len(grid)
-
-
-def replay_cpu(specs, seconds: float, threads: int):
-    """Oracle port (oracle/strait_replay_oracle.c, OpenMP over replays) on an
-    evenly strided subset of the sweep holding ~`seconds` of host work."""
-    from oracle import oracle
-    from paper_2604_28175_b200.replay import ReplayBatch
-
-    budget = seconds * 350_000 * threads  # requests, at the oracle's ~350k req/s/core
-    per = max(1, int(ReplayBatch(specs[:1]).N))
-    k = max(1, int(budget // per))
-    sub = specs[:: max(1, len(specs) // k)][:k]
-    batch = ReplayBatch(sub)
-    t0 = time.perf_counter()
-    res = oracle.replay(batch, threads=threads)
-    dt = time.perf_counter() - t0
-    assert (res.counters[:, 0] == 0).all()
-    return batch.N / dt, dt, len(sub), batch.N
-
-
-def replay_leg(args, ws, rank, local, dist):
-    """Device time of the whole C4 sweep (inputs resident in HBM) + the same
-    through the public API end to end (ReplayBatch(specs, generate="device")
-    .run(): host configs in, per-request outcomes + counters + metrics out)."""
-    import ctypes as Cc
-
-    import torch
-
-    from paper_2604_28175_b200 import _device as D
-    from paper_2604_28175_b200.replay import RC, ReplayBatch
-
-    specs, n_total = c4_shard(args, ws, rank)
-    t0 = time.perf_counter()
-    batch = ReplayBatch(specs, generate="device")  # streams drawn on the GPU
-    torch.cuda.synchronize()
-    build_s = time.perf_counter() - t0
-    lib = D.lib()
-    din = batch.device_inputs()
-    dout = batch.alloc_outputs(device=True)
-    cargs = batch.args(din, dout, D.ptr)
-    st0, sp0 = din["pred_state"].clone(), din["pred_step"].clone()
-    stream = torch.cuda.current_stream()
-
-    def launch():
-        din["pred_state"].copy_(st0)
-        din["pred_step"].copy_(sp0)
-        D.check(lib.strait_replay(Cc.byref(cargs), stream.cuda_stream))
-
-    launch()  # warm-up (module load, smem carve-out)
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    l0 = lib.strait_kernel_launches()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    torch.cuda.synchronize()
-    ev[0].record()
-    for _ in range(args.replay_steps):
-        launch()
-    ev[1].record()
-    torch.cuda.synchronize()
-    dev_ms = ev[0].elapsed_time(ev[1]) / args.replay_steps
-    launches = (lib.strait_kernel_launches() - l0) / args.replay_steps
-    counters = D.host(dout["counters"]).reshape(batch.R, -1)
-    assert (counters[:, RC["ERROR"]] == 0).all(), "replay error"
-    # end to end through the public API: ReplayBatch(specs, generate="device").run() — the
-    # stream descriptions and configs go host->device, the arrival / noise streams are drawn
-    # on the GPU (draw-for-draw numpy's), the replays and compute_metrics run there, and the
-    # per-request outcomes + counters + metrics come back.
-    fetch = {"counters", "req_status", "req_violated"}
-    del din, dout, cargs  # the resident-input buffers above are not part of the API call
-    # Steps pipelined through the public API: step i+1's ReplayBatch (host configs,
-    # stream descriptions H2D, device stream generation) is built on a second
-    # stream while step i's launch() runs, and step i's result() copies it back.
-    s_build, s_run = torch.cuda.Stream(), torch.cuda.Stream()
-
-    def build():
-        with torch.cuda.stream(s_build):
-            b = ReplayBatch(specs, generate="device")
-        return b
-
-    def e2e_pipeline(n):
+    state, t = np.concatenate([P_INIT, np.zeros(24)]), 0
+    dt = 0.0
+    for r in range(warmup + steps):
         t0 = time.perf_counter()
-        nxt, res = build(), None
-        for i in range(n):
-            cur = nxt
-            s_run.wait_stream(s_build)
-            with torch.cuda.stream(s_run):
-                pend = cur.launch(stream=s_run, metrics=True)
-            nxt = build() if i + 1 < n else None  # host + devgen of the next step overlap this replay
-            res = pend.result(fetch=fetch)
-            del pend, cur
-        torch.cuda.synchronize()
-        return (time.perf_counter() - t0) * 1e3 / n, res
-
-    e2e_pipeline(1)  # warm-up: module load, pinned staging
-    e2e_ms_step, res2 = e2e_pipeline(4)
-    e2e = [e2e_ms_step]
-    b2 = res2.batch
-    h2d = int(sum(np.asarray(v).nbytes for k, v in b2.inputs.items() if k != "cfg") + len(bytes(b2.inputs["cfg"])))
-    d2h = int(sum(v.nbytes for k, v in res2.a.items() if k in fetch or k.startswith("m_")))
-    hout = {"counters": torch.from_numpy(res2.a["counters"])}
-    c = hout["counters"].numpy().reshape(batch.R, -1)
-    vec = torch.tensor([dev_ms, float(np.mean(e2e)), build_s, 0, 0, 0, 0, 0, 0], dtype=torch.float64, device="cuda")
-    vec[3:] = torch.tensor([batch.N, c[:, RC["HP_ARR"]].sum(), c[:, RC["LP_ARR"]].sum(), c[:, RC["HP_VIOL"]].sum(),
-                            c[:, RC["LP_VIOL"]].sum(), c[:, RC["BATCHES"]].sum()], dtype=torch.float64)
-    if ws > 1:  # the only collective: max of the times, sum of the counters (NCCL)
-        mx, sm = vec[:3].clone(), vec[3:].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        vec = torch.cat([mx, sm])
-    dev_ms, e2e_ms, build_s, n_req, hp_arr, lp_arr, hp_v, lp_v, nb = vec.tolist()
-    out = {"workload": f"C4 load x HP-fraction sweep (BASELINE configs[3]): {n_total} replays of overload.yaml "
-                       f"(3 s, 6 models x 4 GPUs), replay r on rank r mod {ws}",
-           "value": n_req / (dev_ms / 1e3), "unit": REPLAY_UNIT, "ms_per_step": dev_ms, "steps": args.replay_steps,
-           "replays": n_total, "requests": int(n_req), "batches": int(nb), "scaling": "strong",
-           "hp_violation_pct": 100.0 * hp_v / max(hp_arr, 1), "lp_violation_pct": 100.0 * lp_v / max(lp_arr, 1),
-           "e2e": {"value": n_req / (e2e_ms / 1e3), "unit": REPLAY_UNIT, "h2d_bytes_per_step": h2d,
-                   "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                   "path": "ReplayBatch(specs, generate='device').launch() / .result(): configs + stream specs "
-                           "H2D -> device streams -> strait_replay -> device metrics -> D2H outcomes (wall clock); "
-                           "4 steps pipelined (step i+1's batch built on a second stream while step i runs)"},
-           "host_input_build_s": build_s, "gpu_launches": launches,
-           "bound": "latency (one warp per replay); no roofline claim, DESIGN.md 3.3"}
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        rate, dt, nrep, nreq = replay_cpu(specs, args.cpu_seconds, threads)
-        out["cpu_baseline"] = {"value": rate, "unit": REPLAY_UNIT, "cores": threads, "kind": "port",
-                               "sample": f"{nrep} evenly strided replays of the sweep ({nreq} requests) in {dt:.1f}s "
-                                         f"on {threads} threads (oracle/strait_replay_oracle.c)"}
-    return out
+        oracle.sweep(soa, state[:12], threads=threads)
+        state, t, _, _, _ = oracle.refit(state, t, fbs[r % len(fbs)], nm=5)
+        if r >= warmup:
+            dt += time.perf_counter() - t0
+    preds = (soa.n_triples + soa.n_pairs) * steps
+    return preds / dt, dt
 
 
-def run_reference(args):
-    ws, rank, _ = dist_env()
-    if rank != 0:
-        return
-    from paper_2604_28175_b200.microbench import c3_feedback, c3_round
+def c3_parity(soa_h, fbs, dev_rounds, sample_round: int, seed: int):
+    """Device C3 outputs vs the oracle on the SAME inputs: round 0 in full
+    (every segment, pair and float) and a >= 1 % sample of segments of round
+    `sample_round` (params after `sample_round` refits), plus the refit chain's
+    state after every round, all bit-exact.  `dev_rounds[r]` = (params used,
+    outputs, state after) of device round r."""
+    from oracle import oracle
 
-    soa = c3_round(0, n_segments=args.segments)
-    fb = c3_feedback(0)
-    threads = os.cpu_count() or 1
-    t_budget = max(5.0, min(120.0, args.cpu_seconds))
-    per_step = []
-    for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
-        rate, dt, segs = cpu_round_rate(soa, fb, t_budget / 3, threads)
-        per_step.append(rate)
-    value = float(np.median(per_step))
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(per_step),
-        "warmup": 0, "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "impl": "reference", "config": config_block(args, ws),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"oracle/strait_oracle.c sweep+refit over the C3 round, ~{t_budget / 3:.0f}s "
-                                   f"per step on {threads} threads (OpenMP)"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    if not args.no_replay:
-        specs, n_total = c4_shard(args, 1, 0)
-        rate, dt, nrep, nreq = replay_cpu(specs, t_budget / 3, threads)
-        line["replay"] = {"workload": f"C4 sweep ({n_total} replays), evenly strided sample", "value": rate,
-                          "unit": REPLAY_UNIT, "cores": threads, "kind": "port",
-                          "sample": f"{nrep} replays, {nreq} requests, {dt:.1f}s"}
-    print(json.dumps(line), flush=True)
+    threads = host_threads()
+    state, t = np.concatenate([P_INIT, np.zeros(24)]), 0
+    bad = []
+    checked = {"segments_round0": soa_h.n_segments, "refit_rounds": len(dev_rounds)}
+    for r, (P_dev, out_dev, st_dev) in enumerate(dev_rounds):
+        if not np.array_equal(P_dev, state[:12]):
+            bad.append(f"round {r}: params differ")
+        if r == 0 or r == sample_round:
+            if r == 0:
+                ranges = [(0, soa_h.n_segments)]
+            else:
+                rng = np.random.default_rng(seed)
+                n = max(1, soa_h.n_segments // 256)
+                starts = rng.choice(soa_h.n_segments // n, size=4, replace=False) * n
+                ranges = [(int(s), int(s) + n) for s in sorted(starts)]
+                checked[f"segments_round{r}"] = 4 * n
+            for s0, s1 in ranges:
+                ref = oracle.sweep(soa_h, state[:12], threads=threads, seg_range=(s0, s1))
+                G = soa_h.gpus_per_segment
+                for k, v in ref.items():
+                    lo, hi = (s0, s1) if k.startswith("seg") else (s0 * G, s1 * G)
+                    if not np.array_equal(v[lo:hi], out_dev[k][lo:hi], equal_nan=v.dtype.kind == "f"):
+                        bad.append(f"round {r} {k} [{lo}:{hi}]")
+        state, t, _, _, _ = oracle.refit(state, t, fbs[r % len(fbs)], nm=5)
+        if not np.array_equal(state, st_dev):
+            bad.append(f"round {r}: refit state differs")
+    return {"ok": not bad, "checked": checked, "mismatches": bad[:8]}
 
 
-# ----------------------------------------------------------------------------- our arm
-def run_ours(args):
+def c3_leg(args, ws, rank, local, dist, strong: bool):
+    """One C3 timing leg.  weak: rank's own full round; strong: contiguous
+    segment slice [rank*S/N, (rank+1)*S/N) of round 0 (a segment's 64 pairs
+    never split).  Every rank refits the same feedback chain redundantly
+    (deterministic), so the round needs no communication."""
     import torch
-    import torch.distributed as dist
 
     from paper_2604_28175_b200 import _abi
     from paper_2604_28175_b200 import _device as D
     from paper_2604_28175_b200 import sweep as SW
     from paper_2604_28175_b200.microbench import algorithmic_bytes, c3_feedback, c3_round
-    from paper_2604_28175_b200.predictor import InterferencePredictor
+    from paper_2604_28175_b200.predictor import InterferencePredictor, bias_correction_tables
 
-    ws, rank, local = dist_env()
-    # one process per GPU; STRAIT_DIST_BACKEND=gloo (test only) lets several ranks share a GPU
-    backend = os.environ.get("STRAIT_DIST_BACKEND", "nccl")
-    local = local % torch.cuda.device_count() if backend != "nccl" else local
-    torch.cuda.set_device(local)
-    if ws > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
     lib = _abi.lib()
-
-    soa_h = c3_round(rank, n_segments=args.segments)
+    if strong:
+        full = c3_round(0, n_segments=args.segments)
+        s0, s1 = rank * args.segments // ws, (rank + 1) * args.segments // ws
+        soa_h = full.slice_segments(s0, s1)
+        fb_seed = 0
+    else:
+        soa_h = c3_round(rank, n_segments=args.segments)
+        s0, s1 = 0, args.segments
+        fb_seed = rank * 100000
     n_rounds = args.warmup + args.steps
-    # feedback streams of up to 256 distinct rounds, cycled (each round refits on its own 64 samples)
-    fbs = [c3_feedback(rank * 100000 + r) for r in range(min(max(n_rounds, args.e2e_steps + 2), 256))]
+    fbs = [c3_feedback(fb_seed + r) for r in range(min(max(n_rounds, args.e2e_steps + 8), 256))]
     soa = soa_h.to_device()
     pred = InterferencePredictor()
-    P0 = torch.tensor(pred.params.to_vector(), dtype=torch.float64, device="cuda")
-    stateA = torch.tensor(pred.params.to_vector() + pred.opt.m + pred.opt.v, dtype=torch.float64, device="cuda")
-    stateB = stateA.clone()
+    state0 = torch.tensor(pred.params.to_vector() + pred.opt.m + pred.opt.v, dtype=torch.float64, device="cuda")
+    stateA, stateB = state0.clone(), state0.clone()
     step = torch.zeros(1, dtype=torch.int64, device="cuda")
-    from paper_2604_28175_b200.predictor import bias_correction_tables
-
-    b1, b2 = bias_correction_tables(pred.opt.beta1, pred.opt.beta2, n_rounds * 64 + 64)
+    b1, b2 = bias_correction_tables(pred.opt.beta1, pred.opt.beta2, n_rounds * 64 + 64 * 16)
     bc = (D.dev(b1), D.dev(b2))
     dfb = [{k: D.dev(v, torch.int8 if k == "prio" else torch.float64) for k, v in f.items()} for f in fbs]
     out = SW.alloc_outputs(soa)
-    stream = torch.cuda.current_stream()
     np_ = pred.params.n_params()
 
     def one_round(r, cur, nxt, events=None, dsoa=None, dout=None):
@@ -379,6 +265,24 @@ def run_ours(args):
         SW.launch_round(dsoa or soa, cur[:np_], dout or out, args_r)
         if events:
             events[1].record()
+
+    # ---- parity rounds on the exact benched inputs (before timing; same kernel, same launch)
+    dev_rounds = []
+    if not args.no_parity:
+        cur, nxt = stateA, stateB
+        step.zero_()
+        cur.copy_(state0)
+        sample_round = 5
+        for r in range(sample_round + 1):
+            P_used = D.host(cur[:np_]).copy()
+            one_round(r, cur, nxt)
+            torch.cuda.synchronize()
+            keep = r in (0, sample_round)
+            dev_rounds.append((P_used, {k: D.host(v).copy() for k, v in out.items()} if keep else None,
+                               D.host(nxt).copy()))
+            cur, nxt = nxt, cur
+        step.zero_()
+        stateA.copy_(state0)
 
     cur, nxt = stateA, stateB
     for r in range(args.warmup):
@@ -401,12 +305,18 @@ def run_ours(args):
     launches = lib.strait_kernel_launches() - launches0
     elapsed_ms = t_start.elapsed_time(t_end)
     kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
-    path = SW.last_sweep_path()
+    res = {"elapsed_ms": elapsed_ms, "kern_ms": kern_ms, "launches": launches, "clocks": clocks.summary(),
+           "preds": soa_h.n_triples + soa_h.n_pairs, "triples": soa_h.n_triples, "segments": (s0, s1),
+           "alg_bytes": algorithmic_bytes(soa_h), "path": SW.last_sweep_path(), "soa_h": soa_h, "fbs": fbs}
+    if strong:
+        return res
 
-    # end to end through the public API with HOST buffers: the round's snapshot as the host
-    # holds it — profile-indexed (microbench.c3_compact: int16 profile rows + the non-derived
-    # fields, and the profile tables) in pinned memory -> H2D into the packed device snapshot ->
-    # strait_sweep_expand -> strait_round -> D2H of every decision output.
+    # ---- end to end through the C-ABI with HOST buffers: the round's snapshot as the host holds it —
+    # profile-indexed (microbench.c3_compact: int16 profile rows + the non-derived fields, and the
+    # profile tables) in pinned memory -> H2D into the packed device snapshot -> strait_sweep_expand ->
+    # strait_round -> D2H of every decision output.  Steps are pipelined over three streams with
+    # double-buffered device snapshots and outputs: step i's H2D + expand on the copy stream while step
+    # i-1's round runs on the compute stream and step i-2's decisions go back on the D2H stream.
     from paper_2604_28175_b200.microbench import c3_compact
 
     comp = c3_compact(soa_h)
@@ -415,22 +325,17 @@ def run_ours(args):
     prows = {k: pin(comp["fields"][k]) for k in ("ent_row", "cand_row")}
     ptables = {k: pin(v) for k, v in comp["tables"].items()}
     h2d = sum(t.numel() * t.element_size() for d in (pfields, prows, ptables) for t in d.values())
-    # Steps are pipelined over three streams with double-buffered device snapshots and
-    # outputs. Step i's H2D + expand run on the copy stream while step i-1's round runs on
-    # the compute stream and step i-2's decisions go back on the D2H stream. Every step's
-    # copies lie inside the timed region, and the step time is total / steps.
     soa2 = soa_h.to_device()
     bufs = [soa, soa2]
     dtables = [{k: torch.empty_like(v, device="cuda") for k, v in ptables.items()} for _ in range(2)]
     drows = [{k: torch.empty_like(v, device="cuda") for k, v in prows.items()} for _ in range(2)]
     outs = [out, SW.alloc_outputs(soa)]
     host_outs = [{k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in out.items()} for _ in range(2)]
-    host_out = host_outs[0]
-    d2h = sum(t.numel() * t.element_size() for t in host_out.values())
+    d2h = sum(t.numel() * t.element_size() for t in host_outs[0].values())
     s_h2d, s_d2h, s_cmp = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.current_stream()
+    state = {"cur": cur, "nxt": nxt}
 
     def e2e_pipeline(n, first_round):
-        nonlocal cur, nxt
         ev = {k: [torch.cuda.Event() for _ in range(n)] for k in ("h2d", "cmp", "d2h")}
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -447,8 +352,8 @@ def run_ours(args):
             s_cmp.wait_event(ev["h2d"][i])
             if i >= 2:
                 s_cmp.wait_event(ev["d2h"][i - 2])  # outputs b are free once their D2H finished
-            one_round(first_round + i, cur, nxt, dsoa=bufs[b], dout=outs[b])
-            cur, nxt = nxt, cur
+            one_round(first_round + i, state["cur"], state["nxt"], dsoa=bufs[b], dout=outs[b])
+            state["cur"], state["nxt"] = state["nxt"], state["cur"]
             ev["cmp"][i].record(s_cmp)
             with torch.cuda.stream(s_d2h):
                 s_d2h.wait_event(ev["cmp"][i])
@@ -460,62 +365,414 @@ def run_ours(args):
         return t0.elapsed_time(t1) / n
 
     e2e_pipeline(2, 0)  # warms the pinned copies and the second snapshot
-    e2e_step_ms = e2e_pipeline(args.e2e_steps, 2)
-    host_out = host_outs[(args.e2e_steps - 1) % 2]  # the last step's decisions
+    res["e2e_ms"] = e2e_pipeline(args.e2e_steps, 2)
+    res["h2d"], res["d2h"] = h2d, d2h
+    host_out = host_outs[(args.e2e_steps - 1) % 2]
+    res["checksum"] = float(np.nansum(host_out["seg_latency"].numpy())) + float(host_out["seg_gpu"].numpy().sum())
+    if dev_rounds:
+        res["parity"] = c3_parity(soa_h, fbs, dev_rounds, sample_round=5, seed=rank)
+    return res
 
-    preds = predictions_per_round(soa_h)
-    alg_bytes = algorithmic_bytes(soa_h)
-    checksum = float(np.nansum(host_out["seg_latency"].numpy())) + float(host_out["seg_gpu"].numpy().sum())
-    vec = torch.tensor([elapsed_ms, e2e_step_ms, kern_ms, checksum], dtype=torch.float64, device="cuda")
+
+def reduce_max_sum(dist, ws, maxes, sums):
+    """One NCCL all-reduce each: max of the times, sum of the counts."""
+    import torch
+
+    if ws == 1:
+        return list(maxes), list(sums)
+    mx = torch.tensor(maxes, dtype=torch.float64, device="cuda")
+    sm = torch.tensor(sums, dtype=torch.float64, device="cuda")
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    return mx.tolist(), sm.tolist()
+
+
+def reduce_all_ok(dist, ws, ok: bool) -> bool:
+    import torch
+
+    if ws == 1:
+        return ok
+    v = torch.tensor([0.0 if ok else 1.0], device="cuda")
+    dist.all_reduce(v, op=dist.ReduceOp.SUM)
+    return v.item() == 0
+
+
+# ----------------------------------------------------------------------------- replay legs
+REPLAY_COMPARE = ("req_status", "req_violated", "req_completion", "req_batch", "dec_time", "dec_pass", "dec_model",
+                  "dec_size", "dec_gpu", "dec_est_latency", "dec_intf", "b_kernel_start", "b_kernel_end",
+                  "b_completion", "fb_predicted", "fb_actual", "fb_residual", "fb_flags", "cap_time", "cap_gpu",
+                  "cap_pct", "counters", "pred_state", "pred_step")
+
+
+def replay_parity(specs, dev_res, threads: int):
+    """Device results of `specs` (device-generated streams) vs the oracle on
+    host-generated (numpy) streams of the same specs: every per-request,
+    per-decision, per-batch and cap-row array and every counter bit-exact.
+    Returns (verdict, oracle seconds, requests)."""
+    from oracle import oracle
+    from paper_2604_28175_b200.replay import ReplayBatch
+
+    hb = ReplayBatch(specs)
+    t0 = time.perf_counter()
+    ref = oracle.replay(hb, threads=threads)
+    dt = time.perf_counter() - t0
+    bad = []
+    if hb.N != dev_res.batch.N:
+        bad.append(f"request count {hb.N} != {dev_res.batch.N}")
+    else:
+        for r in range(len(specs)):
+            a, b = ref.replay_slice(r), dev_res.replay_slice(r)
+            for k in REPLAY_COMPARE:
+                x, y = np.asarray(a[k]), np.asarray(b[k])
+                if x.shape != y.shape or not np.array_equal(x, y, equal_nan=x.dtype.kind == "f"):
+                    bad.append(f"replay {r}: {k}")
+                    break
+            if len(bad) > 8:
+                break
+    return {"ok": not bad, "replays": len(specs), "requests": int(hb.N), "arrays": len(REPLAY_COMPARE),
+            "mismatches": bad[:8]}, dt, int(hb.N)
+
+
+def expected_requests(cfg) -> float:
+    """Offered requests of a Poisson/uniform workload (the LPT cost proxy)."""
+    return sum(w.rate * cfg.workload.duration_ms / 1000.0 for w in cfg.workload.models.values()
+               if getattr(w, "mode", "poisson") in ("poisson", "uniform"))
+
+
+def time_launches(batch, steps: int, warm: int = 1):
+    """Device time of `steps` launches of the batch's replay kernel, inputs
+    resident in HBM (predictor state restored before each launch)."""
+    import ctypes as Cc
+
+    import torch
+
+    from paper_2604_28175_b200 import _device as D
+    from paper_2604_28175_b200.replay import RC
+
+    lib = D.lib()
+    din = batch.device_inputs()
+    dout = batch.alloc_outputs(device=True)
+    cargs = batch.args(din, dout, D.ptr)
+    st0, sp0 = din["pred_state"].clone(), din["pred_step"].clone()
+    stream = torch.cuda.current_stream()
+
+    def launch():
+        din["pred_state"].copy_(st0)
+        din["pred_step"].copy_(sp0)
+        D.check(lib.strait_replay(Cc.byref(cargs), stream.cuda_stream))
+
+    for _ in range(warm):
+        launch()
+    torch.cuda.synchronize()
+    l0 = lib.strait_kernel_launches()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for _ in range(steps):
+        launch()
+    ev[1].record()
+    torch.cuda.synchronize()
+    counters = D.host(dout["counters"]).reshape(batch.R, -1)
+    assert (counters[:, RC["ERROR"]] == 0).all(), "replay error"
+    return ev[0].elapsed_time(ev[1]) / steps, (lib.strait_kernel_launches() - l0) / steps, counters
+
+
+def c4_leg(args, ws, rank, dist):
+    """BASELINE configs[3]: 8 loads x 8 HP fractions x 16 seeds of overload's
+    3 s horizon.  Replays are assigned longest-first (LPT on the offered
+    request count); each rank runs its share in one launch."""
+    import torch
+
+    from paper_2604_28175_b200.configs import c4_grid
+    from paper_2604_28175_b200.replay import RC, ReplayBatch, ReplaySpec
+    from paper_2604_28175_b200.shard import lpt
+
+    grid = c4_grid(seeds=args.replay_seeds)
+    costs = [expected_requests(c) for c, _ in grid]
+    assign = lpt(costs, ws)
+    specs = [ReplaySpec(*grid[i]) for i in assign[rank]]
+    t0 = time.perf_counter()
+    batch = ReplayBatch(specs, generate="device")  # streams drawn on the GPU
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
     if ws > 1:
-        mx = vec.clone()
-        dist.all_reduce(mx[:3], op=dist.ReduceOp.MAX)
-        sm = vec.clone()
-        dist.all_reduce(sm[3:], op=dist.ReduceOp.SUM)
-        vec = torch.cat([mx[:3], sm[3:]])
-    elapsed_ms, e2e_step_ms, kern_ms_max, checksum = (float(x) for x in vec.tolist())
-    replay = None if args.no_replay else replay_leg(args, ws, rank, local, dist)
+        dist.barrier()
+    dev_ms, launches, counters = time_launches(batch, args.replay_steps)
+    # end to end through the public API, pipelined: step i+1's ReplayBatch (host configs, stream
+    # descriptions H2D, device stream generation) is built on a second stream while step i runs,
+    # and step i's result() copies outcomes + counters + metrics back.
+    fetch = {"counters", "req_status", "req_violated"}
+    s_build, s_run = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def build():
+        with torch.cuda.stream(s_build):
+            return ReplayBatch(specs, generate="device")
+
+    def e2e_pipeline(n):
+        t0 = time.perf_counter()
+        nxt, res = build(), None
+        for i in range(n):
+            cur = nxt
+            s_run.wait_stream(s_build)
+            pend = cur.launch(stream=s_run, metrics=True)
+            nxt = build() if i + 1 < n else None
+            res = pend.result(fetch=fetch)
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) * 1e3 / n, res
+
+    e2e_pipeline(1)
+    e2e_ms, res2 = e2e_pipeline(4)
+    b2 = res2.batch
+    h2d = int(sum(np.asarray(v).nbytes for k, v in b2.inputs.items() if k != "cfg") + len(bytes(b2.inputs["cfg"])))
+    d2h = int(sum(v.nbytes for k, v in res2.a.items() if k in fetch or k.startswith("m_")))
+    # parity: all of this rank's replays (full outputs of one more device run) vs the oracle
+    par, cpu_dt, cpu_req = None, None, None
+    if not args.no_parity:
+        full = ReplayBatch(specs, generate="device").run(metrics=False)
+        par, cpu_dt, cpu_req = replay_parity(specs, full, host_threads())
+    ok = reduce_all_ok(dist, ws, par is None or par["ok"])
+    c = counters
+    mx, sm = reduce_max_sum(dist, ws, [dev_ms, e2e_ms, build_s],
+                            [batch.N, c[:, RC["HP_ARR"]].sum(), c[:, RC["LP_ARR"]].sum(), c[:, RC["HP_VIOL"]].sum(),
+                             c[:, RC["LP_VIOL"]].sum(), c[:, RC["BATCHES"]].sum()])
+    dev_ms, e2e_ms, build_s = mx
+    n_req, hp_arr, lp_arr, hp_v, lp_v, nb = sm
+    # predicted critical path per rank: the longest replay (one warp's serial chain) vs the rank's
+    # whole share at the measured aggregate rate
+    per_rank = [{"replays": len(a), "offered_requests": int(sum(costs[i] for i in a)),
+                 "longest_replay_requests": int(max((costs[i] for i in a), default=0))} for a in assign]
+    out = {"workload": f"C4 load x HP-fraction sweep (BASELINE configs[3]): {len(grid)} replays of overload.yaml "
+                       f"(3 s, 6 models x 4 GPUs), LPT-assigned over {ws} rank(s)",
+           "value": n_req / (dev_ms / 1e3), "unit": REPLAY_UNIT, "ms_per_step": dev_ms, "steps": args.replay_steps,
+           "replays": len(grid), "requests": int(n_req), "batches": int(nb), "scaling": "strong",
+           "hp_violation_pct": 100.0 * hp_v / max(hp_arr, 1), "lp_violation_pct": 100.0 * lp_v / max(lp_arr, 1),
+           "e2e": {"value": n_req / (e2e_ms / 1e3), "unit": REPLAY_UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                   "path": "ReplayBatch(specs, generate='device').launch() / .result(): configs + stream specs "
+                           "H2D -> device streams -> strait_replay -> device metrics -> D2H outcomes (wall clock); "
+                           "4 steps pipelined (step i+1's batch built on a second stream while step i runs)"},
+           "host_input_build_s": build_s, "gpu_launches": launches, "assignment": {"policy": "LPT", "ranks": per_rank},
+           "bound": "latency (one warp per replay); no roofline claim, DESIGN.md 3.3"}
+    if par is not None:
+        out["parity"] = dict(par, ok=ok)
+        if rank == 0 and ws == 1:
+            out["cpu_baseline"] = {"value": cpu_req / cpu_dt, "unit": REPLAY_UNIT, "cores": host_threads(),
+                                   "kind": "port", "sample": f"all {len(specs)} replays ({cpu_req} requests, the "
+                                   f"whole workload) in {cpu_dt:.1f}s (oracle/strait_replay_oracle.c, OpenMP over "
+                                   f"replays; the run that the parity check compares against)"}
+    return out
+
+
+def single_leg(name, cfg_fn, args, ws, rank, dist, label, steps=1, warm=0, warm_cfg=None, extrapolate_to=None):
+    """One replay per rank (replicas only): rank r runs seed
+    base + r.  Device time of the resident-input launch, e2e through
+    ReplayBatch(..., generate='device').run(), parity of rank 0's replay vs
+    the oracle, and the oracle's single-core rate on the same replay."""
+    import torch
+
+    from paper_2604_28175_b200.replay import RC, ReplayBatch, ReplaySpec
+
+    cfg = cfg_fn()
+    spec = ReplaySpec(cfg, cfg.seed + rank)
+    if warm_cfg is not None:  # load the kernel instantiation on a short slice
+        time_launches(ReplayBatch([ReplaySpec(warm_cfg(), cfg.seed + rank)], generate="device"), 1, warm=0)
+    batch = ReplayBatch([spec], generate="device")
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    dev_ms, launches, counters = time_launches(batch, steps, warm=warm)
+    t0 = time.perf_counter()
+    res = ReplayBatch([spec], generate="device").run(metrics=True)
+    torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    h2d = int(sum(np.asarray(v).nbytes for k, v in res.batch.inputs.items() if k != "cfg"))
+    d2h = int(sum(v.nbytes for v in res.a.values()))
+    par = cpu = None
+    if not args.no_parity and rank == 0:
+        par, cpu_dt, cpu_req = replay_parity([spec], res, 1)
+        cpu = {"value": cpu_req / cpu_dt, "unit": REPLAY_UNIT, "cores": 1, "kind": "port",
+               "sample": f"the same replay ({cpu_req} requests) on 1 core in {cpu_dt:.1f}s "
+                         f"(oracle/strait_replay_oracle.c; a replay is sequential)"}
+    ok = reduce_all_ok(dist, ws, par is None or par["ok"])
+    c = counters[0]
+    mx, sm = reduce_max_sum(dist, ws, [dev_ms, e2e_ms], [batch.N])
+    dev_ms, e2e_ms = mx
+    n_req = sm[0]
+    out = {"workload": label, "value": n_req / (dev_ms / 1e3), "unit": REPLAY_UNIT, "ms_per_step": dev_ms,
+           "steps": steps, "requests_per_replica": int(batch.N), "replicas": ws,
+           "scaling": "weak (replicas only: one replay cannot be split, SURVEY §8(e))",
+           "hp_violation_pct": 100.0 * c[RC["HP_VIOL"]] / max(c[RC["HP_ARR"]], 1),
+           "lp_violation_pct": 100.0 * c[RC["LP_VIOL"]] / max(c[RC["LP_ARR"]], 1),
+           "batches": int(c[RC["BATCHES"]]), "gpu_launches": launches,
+           "e2e": {"value": n_req / (e2e_ms / 1e3), "unit": REPLAY_UNIT, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                   "path": "ReplayBatch([spec], generate='device').run(): config + stream specs H2D -> device "
+                           "streams -> strait_replay -> device metrics -> every output array D2H (wall clock)"}}
+    if par is not None:
+        out["parity"] = dict(par, ok=ok)
+    if cpu is not None:
+        out["cpu_baseline"] = cpu
+    if extrapolate_to:
+        rate = batch.N / (dev_ms / 1e3)
+        out["extrapolated"] = {"requests": extrapolate_to, "device_minutes": extrapolate_to / rate / 60.0,
+                               "note": f"linear extrapolation of the timed {batch.N}-request prefix to the full "
+                                       f"{extrapolate_to / 1e6:.0f}M-request replay (not a measurement)"}
+        if cpu:
+            out["extrapolated"]["cpu_port_minutes_1core"] = extrapolate_to / cpu["value"] / 60.0
+    return out
+
+
+def c5_full_leg(rank):
+    """The whole ~100M-request C5 replay on the device (optional: ~20 min)."""
+    from paper_2604_28175_b200.configs import C5_DURATION_MS, c5_prefix
+    from paper_2604_28175_b200.replay import RC, ReplayBatch, ReplaySpec
+
+    cfg = c5_prefix(duration=C5_DURATION_MS)
+    batch = ReplayBatch([ReplaySpec(cfg, cfg.seed + rank)], generate="device")
+    dev_ms, launches, counters = time_launches(batch, 1, warm=0)
+    c = counters[0]
+    return {"workload": "C5 full: 64 GPUs, 20 models, bursty HP, 1,923 s", "requests": int(batch.N),
+            "value": batch.N / (dev_ms / 1e3), "unit": REPLAY_UNIT, "ms": dev_ms,
+            "hp_violation_pct": 100.0 * c[RC["HP_VIOL"]] / max(c[RC["HP_ARR"]], 1),
+            "lp_violation_pct": 100.0 * c[RC["LP_VIOL"]] / max(c[RC["LP_ARR"]], 1)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The reference path's CPU implementation on the box's host cores: the
+    oracle port's sweep + refit over the full C3 round, every step one whole
+    round (the same work as one of our steps), all host threads.  Maps no
+    product code: only oracle/build/libstrait_oracle.so."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2604_28175_b200.microbench import c3_feedback, c3_round
+
+    soa = c3_round(0, n_segments=args.segments)
+    fbs = [c3_feedback(r) for r in range(min(args.warmup + args.steps, 256))]
+    threads = host_threads()
+    value, dt = cpu_rounds(soa, fbs, args.steps, args.warmup, threads)
+    libs = loaded_repo_libs()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference", "config": config_block(args, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"oracle/strait_oracle.c sweep + refit, {args.steps} timed full C3 rounds "
+                                   f"({soa.n_segments} segments each) after {args.warmup} warm-up rounds on "
+                                   f"{threads} threads (OpenMP)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "same_steps": True, "native_so_loaded": libs,
+        "reference_note": "the reference (pkg/src/infersim) is pure Python and cannot run on the GPU box; "
+                          "its CPU path is timed as the plain-C port that reproduces it bit for bit",
+    }
+    assert all(p.startswith("oracle/") for p in libs), f"reference arm mapped product code: {libs}"
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    # one process per GPU; STRAIT_DIST_BACKEND=gloo (test only) lets several ranks share a GPU
+    backend = os.environ.get("STRAIT_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend != "nccl" else local
+    torch.cuda.set_device(local)
+    if ws > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+
+    weak = c3_leg(args, ws, rank, local, dist, strong=False)
+    mx, sm = reduce_max_sum(dist, ws, [weak["elapsed_ms"], weak["e2e_ms"], weak["kern_ms"]], [weak["checksum"]])
+    elapsed_ms, e2e_step_ms, kern_ms_max = mx
+    c3_ok = reduce_all_ok(dist, ws, "parity" not in weak or weak["parity"]["ok"])
+    strong = c3_leg(args, ws, rank, local, dist, strong=True)
+    smx, ssm = reduce_max_sum(dist, ws, [strong["elapsed_ms"]], [strong["preds"]])
+    legs = {}
+    if not args.no_replay:
+        legs["c4"] = c4_leg(args, ws, rank, dist)
+    if not args.no_single:
+        from paper_2604_28175_b200.configs import C5_DURATION_MS, c1, c2, c5_prefix, overload
+
+        legs["c1"] = single_leg("c1", c1, args, ws, rank, dist,
+                                "C1 (BASELINE configs[0]): demo.yaml minus the uniform stream, 1 GPU, 2 models, "
+                                "26.3 s, ~9.9k requests", steps=3, warm=1)
+        legs["c2"] = single_leg("c2", c2, args, ws, rank, dist,
+                                "C2 (BASELINE configs[1]): overload.yaml at 166.7 s, 6 models x 4 GPUs, ~1.0M "
+                                "requests", warm_cfg=lambda: overload(300))
+        legs["c5"] = single_leg("c5", c5_prefix, args, ws, rank, dist,
+                                "C5 (BASELINE configs[4]) prefix: the first 19.23 s (~1.0M requests) of the "
+                                "1,923 s / ~100M-request replay on 64 GPUs x 20 models",
+                                warm_cfg=lambda: c5_prefix(duration=200.0),
+                                extrapolate_to=int(1e8))
+        if args.c5_full:
+            legs["c5_full"] = c5_full_leg(rank)
     if rank != 0:
         if ws > 1:
             dist.destroy_process_group()
         return
+
     ms_per_step = elapsed_ms / args.steps
+    preds = weak["preds"]
     value = ws * preds * args.steps / (elapsed_ms / 1e3)
     peaks_path = os.path.join(REPO, "MEASURED_PEAKS.json")
     peak, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
     if os.path.exists(peaks_path):
         peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
-    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-    traffic = None
+    kern_ms = weak["kern_ms"]
+    achieved = weak["alg_bytes"] / (kern_ms / 1e3) / 1e9
+    survey_bytes = 89 * weak["triples"] + 114 * (weak["triples"] // 4) + 101 * (weak["triples"] // 256)
+    traffic, traffic_src = None, None
     tfile = os.path.join(REPO, "profiles", "sweep_traffic.json")
     if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+        t = json.load(open(tfile))
+        traffic = t.get("dram_bytes_per_launch")
+        traffic_src = f"stored ncu --set full capture ({t.get('source', 'profiles/')}), not measured in this run"
+    parity = {"c3_round0": weak.get("parity", {}).get("ok") if "parity" in weak else None}
+    parity["c3_round0"] = c3_ok if "parity" in weak else None
+    for k, v in legs.items():
+        if isinstance(v, dict) and "parity" in v:
+            parity[k] = v["parity"]["ok"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "impl": "ours",
         "config": config_block(args, ws),
-        "triples_per_s": ws * soa_h.n_triples * args.steps / (elapsed_ms / 1e3),
-        "e2e": {"value": ws * preds / (e2e_step_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_step_ms,
+        "triples_per_s": ws * weak["triples"] * args.steps / (elapsed_ms / 1e3),
+        "e2e": {"value": ws * preds / (e2e_step_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": weak["h2d"],
+                "d2h_bytes_per_step": weak["d2h"], "ms_per_step": e2e_step_ms,
                 "path": "pinned profile-indexed snapshot (int16 profile rows + non-derived fields + profile "
                         "tables) -> H2D -> strait_sweep_expand -> strait_round (C-ABI) -> D2H decisions; "
                         f"{args.e2e_steps} steps pipelined over copy/compute/D2H streams, total / steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_source": peak_src, "kernel": f"strait_round ({path} sweep path)",
-                     "algorithmic_bytes_per_launch": alg_bytes, "kernel_ms": kern_ms},
-        "gpu_launches": int(launches),
-        "clocks": clocks.summary(),
-        "replay": replay,
-        "checksum": checksum,
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
+                     "kernel": f"strait_round ({weak['path']} sweep path)",
+                     "algorithmic_bytes_per_launch": weak["alg_bytes"],
+                     "bytes_basis": "121 B/triple + 114 B/pair + 109 B/segment: the triple record carries twa[5] "
+                                    "(40 B), because intf_cur depends on the round's refit params (DESIGN.md 3.1)",
+                     "frac_survey_basis": survey_bytes / (kern_ms / 1e3) / 1e9 / peak,
+                     "survey_bytes_per_launch": survey_bytes, "kernel_ms": kern_ms},
+        "gpu_launches": int(weak["launches"]),
+        "clocks": weak["clocks"],
+        "parity": parity,
+        "c3_parity_detail": weak.get("parity"),
+        "c3_strong": {"workload": f"C3 round 0 ({args.segments} segments) split into {ws} contiguous slices of whole "
+                                  "segments; the feedback chain refit redundantly on every rank",
+                      "value": ssm[0] * args.steps / (smx[0] / 1e3), "unit": UNIT, "ms_per_step": smx[0] / args.steps,
+                      "scaling": "strong", "segments_rank0": list(strong["segments"])},
+        "checksum": sm[0],
+        "native_so_loaded": loaded_repo_libs(),
+        **legs,
     }
     if not args.no_cpu_baseline:
-        from paper_2604_28175_b200.microbench import c3_feedback as _fb
-
-        threads = os.cpu_count() or 1
-        rate, dt, segs = cpu_round_rate(soa_h, _fb(0), args.cpu_seconds, threads)
+        threads = host_threads()
+        nsteps = max(1, min(args.steps, int(args.cpu_seconds / 0.08)))
+        rate, dt = cpu_rounds(weak["soa_h"], weak["fbs"], nsteps, 1, threads)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                                "sample": f"oracle sweep+refit, {segs} segments of the C3 round in {dt:.1f}s"}
+                                "sample": f"oracle sweep + refit, {nsteps} full C3 rounds in {dt:.1f}s"}
     print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()

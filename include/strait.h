@@ -62,12 +62,6 @@ int64_t strait_kernel_launches(void);
  * 1 synchronous, 2 bulk-copy pipeline, 3 tensor-map pipeline */
 int strait_last_sweep_path(void);
 
-/* HOST utility for input preparation: y[i] = exp(x[i]) with the host C
- * library, i.e. the same libm call as Python's math.exp — used to turn the
- * reference's normal draws into its lognormal batch noise exactly
- * (simulation.py:309-311).  Not a device path. */
-void strait_host_exp(const double *x, double *y, int64_t n);
-
 /*
  * Elementwise device math with the reference host's bits: fn 0 exp(x),
  * 1 log(x), 2 pow(x, y), 3 log1p(x) — restatements of glibc 2.39's

@@ -36,6 +36,8 @@ def lib():
 
         _lib.oracle_replay.argtypes = [C.POINTER(ReplayArgs), C.c_int]
         _lib.oracle_replay.restype = C.c_int
+        _lib.oracle_exp.argtypes = [vp, vp, C.c_int64]
+        _lib.oracle_exp.restype = None
     return _lib
 
 
@@ -122,12 +124,22 @@ def refit(state, step, samples, *, nm, cap=50.0, lr=0.0075, beta1=0.7, beta2=0.9
     return state, int(stepa[0]), pred, res, flags
 
 
+def exp(z):
+    """glibc exp elementwise (the reference's math.exp)."""
+    z = _f64(z)
+    out = np.empty_like(z)
+    lib().oracle_exp(_p(z), _p(out), z.size)
+    return out
+
+
 def replay(batch, threads=1):
     """Reference discrete-event replay (oracle/strait_replay_oracle.c) of a
     paper_2604_28175_b200.replay.ReplayBatch on host buffers."""
     from paper_2604_28175_b200.replay import ReplayResult
 
     inputs = batch.host_inputs()
+    if "noise_z" in inputs:  # host-drawn normals -> math.exp(z) with glibc (simulation.py:309-311)
+        inputs["noise"] = exp(inputs.pop("noise_z"))
     inputs["pred_state"] = inputs["pred_state"].copy()
     inputs["pred_step"] = inputs["pred_step"].copy()
     outputs = batch.alloc_outputs(device=False)

@@ -245,3 +245,9 @@ int oracle_refit(const StraitRefitArgs *a) {
   }
   return 0;
 }
+
+/* simulation.py:309-311: the per-batch noise factor math.exp(normal(0, sigma)),
+ * applied to host-drawn normals with glibc exp (the same call as math.exp). */
+void oracle_exp(const double *z, double *out, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) out[i] = exp(z[i]);
+}

@@ -246,8 +246,8 @@ static void pred_update(Sim *S, const double *twa, double cmp, double mem, int p
   *predicted = pred;
   *residual = res;
   *saturated = sat;
-  *skipped = !finite;
-  if (!finite) return;
+  *skipped = !finite && !S->cfg->refit_frozen;
+  if (!finite || S->cfg->refit_frozen) return; /* frozen update(): loss terms only, never steps */
   int64_t t = ++S->step;
   double b1 = S->cfg->beta1, b2 = S->cfg->beta2;
   double bc1 = 1.0 - pow(b1, (double)t), bc2 = 1.0 - pow(b2, (double)t);

@@ -170,8 +170,6 @@ def _declare(lib):
     lib.strait_gt_slowdown.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, C.c_int64, _vp, _vp]
     lib.strait_sweep_expand.restype = C.c_int
     lib.strait_sweep_expand.argtypes = [C.POINTER(SweepExpandArgs), C.POINTER(SweepArgs), _vp]
-    lib.strait_host_exp.restype = None
-    lib.strait_host_exp.argtypes = [_vp, _vp, C.c_int64]
     if hasattr(lib, "strait_replay"):
         from ._replay_abi import declare_replay
 

@@ -23,7 +23,8 @@ class ReplayModels(C.Structure):
 class ReplayConfig(C.Structure):
     _fields_ = [("n_gpus", C.c_int32), ("concurrency_limit", C.c_int32), ("use_priority_order", C.c_int32),
                 ("use_meet", C.c_int32), ("use_violate", C.c_int32), ("gt_family", C.c_int32),
-                ("has_noise", C.c_int32), ("policy", C.c_int32),
+                ("has_noise", C.c_int32), ("policy", C.c_int32), ("refit_frozen", C.c_int32),
+                ("reserved0", C.c_int32),
                 ("effect_cap", C.c_double), ("learning_rate", C.c_double), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("eps", C.c_double), ("huber_delta", C.c_double),
                 ("gt_scale", C.c_double), ("gt_base", C.c_double), ("gt_offset", C.c_double),

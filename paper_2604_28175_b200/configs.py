@@ -98,6 +98,18 @@ def c4_grid(duration=3000, seeds=C4_SEEDS):
     return out
 
 
+C5_DURATION_MS = 1_923_000.0  # >= 33 trace minutes: ~100M requests
+C5_MINUTES = 33
+C5_PREFIX_MS = 19_230.0  # the first ~1.0M requests of that replay
+
+
+def c5_prefix(duration=C5_PREFIX_MS, seed=0):
+    """The timed prefix of the 100M-request C5 replay: the full run's inputs
+    (33-minute trace table, same RNG consumption), cut at `duration` — its
+    arrivals, and so its decisions, are the full run's first ones."""
+    return c5(duration=duration, minutes=C5_MINUTES, seed=seed)
+
+
 def c5(duration=150.0, minutes=2, seed=0, n_gpus=64):
     """C5 shape: 20 random_profile models (m00-m05 HP bursty
     trace, m06-m19 LP Poisson 2600/s), 64 GPUs."""

@@ -52,7 +52,3 @@ extern "C" int64_t strait_struct_size(int32_t id) {
 }
 extern "C" const char* strait_last_error(void) { return g_err; }
 extern "C" int64_t strait_kernel_launches(void) { return g_launches.load(); }
-
-extern "C" void strait_host_exp(const double* x, double* y, int64_t n) {
-  for (int64_t i = 0; i < n; ++i) y[i] = ::exp(x[i]);
-}

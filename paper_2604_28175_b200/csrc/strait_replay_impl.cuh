@@ -567,8 +567,9 @@ struct Sim : Geom<GEOM> {
     const double gh = fabs(residual) <= delta ? residual : (residual > 0 ? delta : -delta);
     const double gk = gh * d;
     const bool finite = __all_sync(kFull, !owner || isfinite(gk)) && isfinite(residual);
-    skipped = !finite;
-    if (!finite) return;  // UpdateResult(skipped=True)
+    skipped = !finite && !cf->refit_frozen;
+    // UpdateResult(skipped=True); a frozen update() returns the loss terms and never steps
+    if (!finite || cf->refit_frozen) return;
     ++step;               // adam_step (predictor.py:124-145)
     const double bc1 = step <= A->n_bc ? __ldg(&A->bc1[step - 1]) : 1.0;
     const double bc2 = step <= A->n_bc ? __ldg(&A->bc2[step - 1]) : 1.0;

@@ -12,6 +12,7 @@ host<->device round trip over many samples.
 from __future__ import annotations
 
 import ctypes as C
+import copy
 import json
 import math
 from dataclasses import dataclass, field
@@ -470,3 +471,56 @@ class InterferencePredictor:
     def load(cls, path) -> "InterferencePredictor":
         with open(path) as f:
             return cls.from_checkpoint_dict(json.load(f))
+
+
+# ----------------------------------------------------------------------------- injection seam
+
+_ENGINE_METHODS = ("predict", "predict_batch", "estimate_latency")
+
+
+def refit_mode(predictor: InterferencePredictor) -> str:
+    """How the device replay engine runs an injected predictor
+    (``Simulation(config, predictor=...)``, simulation.py:127,155).
+
+    The engine evaluates the stock estimator and refit on the device, so an
+    injected object is accepted only where that is exactly what the object
+    does; anything else raises instead of being silently replaced:
+
+    * ``"adam"``: ``update`` is the stock Adam/Huber step (predictor.py:345-363),
+      inherited or overridden with the same effect;
+    * ``"frozen"``: ``update`` evaluates the loss but never changes ``params``
+      or ``opt`` — the reference's own FrozenPredictor
+      (tests/test_simulation.py:316-323);
+    * ``NotImplementedError`` for overridden ``predict``/``estimate_latency`` or
+      any other ``update``.
+
+    An overridden ``update`` is classified by running it on copies of the
+    predictor over probe samples and comparing the resulting state with the
+    stock update's.
+    """
+    cls = type(predictor)
+    for name in _ENGINE_METHODS:
+        if getattr(cls, name) is not getattr(InterferencePredictor, name):
+            raise NotImplementedError(f"{cls.__name__}.{name} is overridden; the device replay engine evaluates "
+                                      f"the stock estimator (predictor.py:208-242) and cannot run it")
+    if cls.update is InterferencePredictor.update:
+        return "adam"
+    nm = len(predictor.params.weights)
+    probes = [FeedbackSample(f"probe{i}", tuple(0.1 * (i + 1 + k) for k in range(nm)), 0.2 + 0.1 * i,
+                             0.3, PriorityLevel(i % 2), 1.0 + 0.7 * i) for i in range(3)]
+
+    def state(p):
+        return (p.params.to_vector(), list(p.opt.m), list(p.opt.v), p.opt.step)
+
+    custom, stock = copy.deepcopy(predictor), copy.deepcopy(predictor)
+    before = state(custom)
+    for smp in probes:
+        custom.update(smp)
+        InterferencePredictor.update(stock, smp)
+    after = state(custom)
+    if after == before:
+        return "frozen"
+    if after == state(stock):
+        return "adam"
+    raise NotImplementedError(f"{cls.__name__}.update changes the predictor differently from the stock "
+                              f"Adam/Huber refit (predictor.py:345-363); the device replay engine cannot run it")

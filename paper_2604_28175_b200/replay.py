@@ -23,7 +23,7 @@ from ._replay_abi import (ARG_ARRAYS, METRIC_OUTPUTS, MS_N, POLICY_CODES, RC, RC
                           ReplayConfig, ReplayModels, TRACE_DTYPE)
 from .config import ExperimentConfig
 from .domain import PriorityLevel
-from .predictor import InterferencePredictor, PredictorParams, bias_correction_tables
+from .predictor import InterferencePredictor, PredictorParams, bias_correction_tables, refit_mode
 
 NOISE_STREAM = 1_000_003  # simulation.py:163
 
@@ -50,12 +50,13 @@ class ReplaySpec:
     predictor: Optional[InterferencePredictor] = None
 
 
-def host_exp(x: np.ndarray) -> np.ndarray:
-    """exp with the host libm (same call as Python's math.exp)."""
-    x = np.ascontiguousarray(x, dtype=np.float64)
-    y = np.empty_like(x)
-    D.lib().strait_host_exp(x.ctypes.data, y.ctypes.data, x.size)
-    return y
+def device_exp(z: torch.Tensor) -> torch.Tensor:
+    """exp of a device array with the glibc-exact device exp (strait_math fn 0,
+    csrc/strait_libm.cuh): the bits of the reference's ``math.exp``
+    (simulation.py:309-311)."""
+    out = torch.empty_like(z)
+    D.check(D.lib().strait_math(0, D.ptr(z), None, z.numel(), D.ptr(out), D.stream_handle()))
+    return out
 
 
 def model_tables(profiles: dict) -> dict:
@@ -80,6 +81,17 @@ def model_tables(profiles: dict) -> dict:
     t["deadline"] = np.array([profiles[i].deadline_ms for i in ids], dtype=np.float64)
     t["timeout"] = np.array([profiles[i].batch_timeout_ms for i in ids], dtype=np.float64)
     return dict(ids=ids, M=M, nm=nm, B=B, **t)
+
+
+def _check_predictor(pred: InterferencePredictor, nm: int) -> None:
+    """The engine reads 3 * (nm + 7) doubles of predictor state per replay; a
+    predictor sized for another metric count raises, as the reference's
+    pressure_exponent does on a metric-count mismatch (predictor.py:169-172)."""
+    n = pred.params.n_params()
+    if n != nm + 7:
+        raise ValueError(f"predictor has {n - 7} metric weights, the profiles have {nm} metrics")
+    if not (len(pred.opt.m) == len(pred.opt.v) == n):
+        raise ValueError(f"optimizer moments have {len(pred.opt.m)}/{len(pred.opt.v)} entries, expected {n}")
 
 
 # baselines.py defaults: StaticSpatialPolicy(cap=3), ReactiveState() (lines 62-110)
@@ -150,8 +162,10 @@ class ReplayBatch:
             cfg = s.config
             seed = cfg.seed if s.seed is None else s.seed
             pred = s.predictor or InterferencePredictor(PredictorParams(weights=(0.1,) * nm))
+            _check_predictor(pred, nm)
             self.preds.append(pred)
             cfgs.append(replay_config(cfg, pred))
+            cfgs[-1].refit_frozen = int(s.predictor is not None and refit_mode(pred) == "frozen")
             states.append(pred.params.to_vector() + list(pred.opt.m) + list(pred.opt.v))
             steps.append(pred.opt.step)
             if generate == "device":
@@ -173,9 +187,10 @@ class ReplayBatch:
             n = len(times)
             if cfg.ground_truth.noise_sigma > 0 and n:
                 rng = np.random.default_rng(np.random.SeedSequence([seed, NOISE_STREAM]))
-                noise.append(host_exp(rng.normal(0.0, cfg.ground_truth.noise_sigma, n)))
+                # the normal draws; exp(z) is applied on the device (device_inputs), bit-exact
+                noise.append(rng.normal(0.0, cfg.ground_truth.noise_sigma, n))
             else:
-                noise.append(np.ones(n))
+                noise.append(np.zeros(n))  # exp(0.0) == 1.0: the reference's noise-free factor
             req_off.append(base + n)
         if generate == "device":
             from . import devgen
@@ -215,7 +230,7 @@ class ReplayBatch:
         }
         if generate == "host":
             self.inputs.update(arr_time=np.concatenate(arr_t), arr_model=np.concatenate(arr_m),
-                               model_req=np.concatenate(model_req), noise=np.concatenate(noise))
+                               model_req=np.concatenate(model_req), noise_z=np.concatenate(noise))
 
     # ------------------------------------------------------------------ buffers
     def alloc_outputs(self, device: bool):
@@ -263,6 +278,9 @@ class ReplayBatch:
         return d
 
     def host_inputs(self) -> dict:
+        """Host copies of the inputs.  Host-drawn batches hold the noise as the
+        normal draws ``noise_z`` (the factor is exp(z), applied where the replay
+        runs); device-generated batches hold the factors ``noise``."""
         d = self._host_small()
         for k, v in self._dev.items():  # device-generated streams (copied back for host checkers)
             d[k] = D.host(v)[:max(self.N, 1)]
@@ -282,6 +300,8 @@ class ReplayBatch:
         for k, t in out.items():
             if isinstance(t, torch.Tensor) and not t.numel():
                 out[k] = D.empty(1, t.dtype)
+        if "noise_z" in out:  # host-drawn normals -> the per-batch factors exp(z), on the device
+            out["noise"] = device_exp(out.pop("noise_z"))
         return out
 
     # ------------------------------------------------------------------ metrics
@@ -314,74 +334,89 @@ class ReplayBatch:
                  "kernel_overhead": (max(self.N, 1), torch.float64)}
         return {k: D.empty(n, dt) for k, (n, dt) in sizes.items()}
 
-    def launch(self, stream=None, metrics: bool = True) -> "PendingReplay":
-        """Enqueue the replay (+ device metrics) without waiting: the host is
-        free to build the next batch while this one runs (`PendingReplay.result`
-        collects it).  Untraced batches only (a trace may need a re-run)."""
-        if self.trace:
-            raise ValueError("launch() is for untraced batches; use run() with trace=True")
+    def _enqueue(self, metrics: bool):
+        """Inputs, outputs, replay and metrics launches, all on the current stream."""
         din = self.device_inputs()
         dout = self.alloc_outputs(device=True)
         args = self.args(din, dout, D.ptr)
-        D.check(D.lib().strait_replay(C.byref(args), D.stream_handle(stream)))
+        D.check(D.lib().strait_replay(C.byref(args), D.stream_handle()))
         mout = None
         if metrics:
             din["window_ms"] = D.dev(np.array([s.config.goodput_window_ms for s in self.specs], dtype=np.float64))
             mout = self.alloc_metrics()
             margs = self.metrics_args(din, dout, mout, D.ptr)
-            D.check(D.lib().strait_replay_metrics(C.byref(margs), D.stream_handle(stream)))
-        return PendingReplay(self, din, dout, mout, stream)
+            D.check(D.lib().strait_replay_metrics(C.byref(margs), D.stream_handle()))
+        return din, dout, mout
 
-    def run(self, stream=None, metrics: bool = True, fetch=None) -> "ReplayResult":
-        """Host in, device replay (+ device metrics), host out.  `fetch`
-        limits the device->host copy to those output arrays (default: all)."""
-        din = self.device_inputs()
-        dout = self.alloc_outputs(device=True)
-        args = self.args(din, dout, D.ptr)
-        D.check(D.lib().strait_replay(C.byref(args), D.stream_handle(stream)))
-        if self.trace:  # an event log that overflowed: re-run with the exact capacity
-            need = int(D.host(dout["counters"]).reshape(self.R, RC_N)[:, RC["TRACE"]].max())
+    def _overflow(self, counters: np.ndarray) -> bool:
+        """Grow the cap-row / event-log capacity if a replay overflowed it
+        (the kernel counts every row but stores only the first `*_max`);
+        True means the launch must be repeated."""
+        c = counters.reshape(self.R, RC_N)
+        grow = False
+        need = int(c[:, RC["CAP_ROWS"]].max()) if self.R else 0
+        if need > self.cap_rows_max:
+            self.cap_rows_max, grow = need, True
+        if self.trace:
+            need = int(c[:, RC["TRACE"]].max())
             if need > self.trace_max:
                 if need > 2**31 - 1:
                     raise ValueError(f"event log of {need} records exceeds the trace capacity")
-                self.trace_max = need
+                self.trace_max, grow = need, True
+        return grow
+
+    def launch(self, stream=None, metrics: bool = True) -> "PendingReplay":
+        """Enqueue the replay (+ device metrics) on `stream` (default: the current
+        stream) without waiting: the host is free to build the next batch while
+        this one runs (`PendingReplay.result` collects it).  Untraced batches
+        only (a trace may need a re-run)."""
+        if self.trace:
+            raise ValueError("launch() is for untraced batches; use run() with trace=True")
+        with _on(stream):
+            din, dout, mout = self._enqueue(metrics)
+        return PendingReplay(self, din, dout, mout, stream, metrics)
+
+    def run(self, stream=None, metrics: bool = True, fetch=None) -> "ReplayResult":
+        """Host in, device replay (+ device metrics), host out, every step on
+        `stream` (default: the current stream).  `fetch` limits the
+        device->host copy to those output arrays (default: all)."""
+        with _on(stream):
+            din, dout, mout = self._enqueue(metrics)
+            if self._overflow(D.host(dout["counters"])):  # cap rows / event log overflowed: exact re-run
                 return self.run(stream, metrics, fetch)
-        res = {}
-        if metrics:
-            din["window_ms"] = D.dev(np.array([s.config.goodput_window_ms for s in self.specs], dtype=np.float64))
-            mout = self.alloc_metrics()
-            margs = self.metrics_args(din, dout, mout, D.ptr)
-            D.check(D.lib().strait_replay_metrics(C.byref(margs), D.stream_handle(stream)))
-            series = ("intf_error", "latency_error", "kernel_overhead")  # per-batch arrays: only on request
-            res.update({"m_" + k: D.host(v) for k, v in mout.items()
-                        if fetch is None or k not in series or "m_" + k in fetch})
-        res.update({k: D.host(v) for k, v in dout.items() if fetch is None or k in fetch or k == "counters"})
-        if "trace" in res:
-            res["trace"] = res["trace"].view(TRACE_DTYPE)
-        res["pred_state"] = D.host(din["pred_state"])
-        res["pred_step"] = D.host(din["pred_step"])
-        return ReplayResult(self, res)
+            return ReplayResult(self, _collect(din, dout, mout, fetch))
+
+
+def _on(stream):
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+
+
+def _collect(din, dout, mout, fetch) -> dict:
+    res = {}
+    if mout is not None:
+        series = ("intf_error", "latency_error", "kernel_overhead")  # per-batch arrays: only on request
+        res.update({"m_" + k: D.host(v) for k, v in mout.items()
+                    if fetch is None or k not in series or "m_" + k in fetch})
+    res.update({k: D.host(v) for k, v in dout.items() if fetch is None or k in fetch or k == "counters"})
+    if "trace" in res:
+        res["trace"] = res["trace"].view(TRACE_DTYPE)
+    res["pred_state"] = D.host(din["pred_state"])
+    res["pred_step"] = D.host(din["pred_step"])
+    return res
 
 
 class PendingReplay:
     """A launched replay batch (ReplayBatch.launch); result() copies it back."""
 
-    def __init__(self, batch, din, dout, mout, stream):
+    def __init__(self, batch, din, dout, mout, stream, metrics=True):
         self.batch, self.din, self.dout, self.mout, self.stream = batch, din, dout, mout, stream
+        self.metrics = metrics
 
     def result(self, fetch=None) -> "ReplayResult":
-        ctx = torch.cuda.stream(self.stream) if self.stream is not None else contextlib.nullcontext()
-        with ctx:
-            res = {}
-            if self.mout is not None:
-                series = ("intf_error", "latency_error", "kernel_overhead")
-                res.update({"m_" + k: D.host(v) for k, v in self.mout.items()
-                            if fetch is None or k not in series or "m_" + k in fetch})
-            res.update({k: D.host(v) for k, v in self.dout.items()
-                        if fetch is None or k in fetch or k == "counters"})
-            res["pred_state"] = D.host(self.din["pred_state"])
-            res["pred_step"] = D.host(self.din["pred_step"])
-        return ReplayResult(self.batch, res)
+        with _on(self.stream):
+            if self.batch._overflow(D.host(self.dout["counters"])):  # cap rows overflowed: exact re-run
+                return self.batch.run(self.stream, self.metrics, fetch)
+            return ReplayResult(self.batch, _collect(self.din, self.dout, self.mout, fetch))
 
 
 class ReplayResult:

@@ -24,6 +24,30 @@ def shard(items: Sequence, world: int, rank: int) -> list:
     return list(items[rank::world])
 
 
+def lpt(costs: Sequence[float], world: int) -> list[list[int]]:
+    """Longest-processing-time-first assignment of independent replays to
+    ranks: replays in decreasing cost, each to the rank with the least
+    assigned cost so far (ties: lowest rank).  Returns each rank's replay
+    indices in decreasing cost."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    order = sorted(range(len(costs)), key=lambda i: (-costs[i], i))
+    load = [0.0] * world
+    out: list[list[int]] = [[] for _ in range(world)]
+    for i in order:
+        r = min(range(world), key=lambda k: (load[k], k))
+        out[r].append(i)
+        load[r] += costs[i]
+    return out
+
+
+def shard_lpt(items: Sequence, costs: Sequence[float], world: int, rank: int) -> list:
+    """This rank's items under lpt()."""
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world of {world}")
+    return [items[i] for i in lpt(costs, world)[rank]]
+
+
 def local_counts(counters: np.ndarray) -> np.ndarray:
     """Sum of the per-replay counters [R, STRAIT_RC_N] over this rank's replays."""
     c = np.asarray(counters).reshape(-1, np.asarray(counters).shape[-1])
