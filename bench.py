@@ -404,6 +404,11 @@ REPLAY_COMPARE = ("req_status", "req_violated", "req_completion", "req_batch", "
                   "cap_pct", "counters", "pred_state", "pred_step")
 
 
+# every counter but EVENTS (5: live events; the oracle also counts the reference's superseded
+# kernel-completes) and TRACE (13)
+COUNTER_COMPARE = [0, 1, 2, 3, 4, 6, 7, 8, 9, 10, 11, 12]
+
+
 def replay_parity(specs, dev_res, threads: int):
     """Device results of `specs` (device-generated streams) vs the oracle on
     host-generated (numpy) streams of the same specs: every per-request,
@@ -424,6 +429,8 @@ def replay_parity(specs, dev_res, threads: int):
             a, b = ref.replay_slice(r), dev_res.replay_slice(r)
             for k in REPLAY_COMPARE:
                 x, y = np.asarray(a[k]), np.asarray(b[k])
+                if k == "counters":  # the device never materialises the reference's stale events (RC EVENTS)
+                    x, y = x[..., COUNTER_COMPARE], y[..., COUNTER_COMPARE]
                 if x.shape != y.shape or not np.array_equal(x, y, equal_nan=x.dtype.kind == "f"):
                     bad.append(f"replay {r}: {k}")
                     break
@@ -435,7 +442,7 @@ def replay_parity(specs, dev_res, threads: int):
 
 def expected_requests(cfg) -> float:
     """Offered requests of a Poisson/uniform workload (the LPT cost proxy)."""
-    return sum(w.rate * cfg.workload.duration_ms / 1000.0 for w in cfg.workload.models.values()
+    return sum(w.rate_per_s * cfg.workload.duration_ms / 1000.0 for w in cfg.workload.models.values()
                if getattr(w, "mode", "poisson") in ("poisson", "uniform"))
 
 
@@ -590,7 +597,7 @@ def single_leg(name, cfg_fn, args, ws, rank, dist, label, steps=1, warm=0, warm_
     if not args.no_parity and rank == 0:
         par, cpu_dt, cpu_req = replay_parity([spec], res, 1)
         cpu = {"value": cpu_req / cpu_dt, "unit": REPLAY_UNIT, "cores": 1, "kind": "port",
-               "sample": f"the same replay ({cpu_req} requests) on 1 core in {cpu_dt:.1f}s "
+               "sample": f"the same replay ({cpu_req} requests) on 1 core in {cpu_dt:.3f}s "
                          f"(oracle/strait_replay_oracle.c; a replay is sequential)"}
     ok = reduce_all_ok(dist, ws, par is None or par["ok"])
     c = counters[0]
