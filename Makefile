@@ -22,6 +22,7 @@ build/%.o: $(CDIR)/%.cu $(COMMON_HDR)
 	$(NVCC) $(NVFLAGS) -dc -o $@ $<
 
 build/strait_sweep.o: $(SWEEP_HDR)
+build/strait_node.o: $(COMMON_HDR) $(CDIR)/strait_node.cuh include/strait_node.h
 build/strait_workload.o: $(COMMON_HDR) $(CDIR)/strait_rng.cuh $(CDIR)/strait_rng_tables.cuh include/strait_replay.h
 $(patsubst $(CDIR)/%.cu,build/%.o,$(wildcard $(CDIR)/strait_replay*.cu)): $(REPLAY_HDR)
 

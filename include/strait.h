@@ -53,7 +53,8 @@ int strait_abi_version(void);
 /* sizeof of each ABI struct, so bindings can verify their mirrors (HOST only):
  * 0 StraitSweepArgs, 1 StraitSweepExpandArgs, 2 StraitRefitArgs, 3 StraitReplayModels,
  * 4 StraitReplayConfig, 5 StraitReplayArgs, 6 StraitTraceRec, 7 StraitMetricsArgs,
- * 8 StraitStreamSpec, 9 StraitGroundTruth; -1 for an unknown id */
+ * 8 StraitStreamSpec, 9 StraitGroundTruth, 10 StraitGpuHdr, 11 StraitNodeEntry, 12 StraitProposeArgs,
+ * 13 StraitProposeOut (strait_node.h); -1 for an unknown id */
 int64_t strait_struct_size(int32_t id);
 const char *strait_last_error(void);
 /* number of device kernels this library launched since load (evidence counter) */

@@ -8,6 +8,7 @@
 #include <cstdio>
 
 #include "strait_capi.cuh"
+#include "../../include/strait_node.h"
 #include "../../include/strait_replay.h"
 
 namespace {
@@ -47,6 +48,10 @@ extern "C" int64_t strait_struct_size(int32_t id) {
     case 7: return sizeof(StraitMetricsArgs);
     case 8: return sizeof(StraitStreamSpec);
     case 9: return sizeof(StraitGroundTruth);
+    case 10: return sizeof(StraitGpuHdr);
+    case 11: return sizeof(StraitNodeEntry);
+    case 12: return sizeof(StraitProposeArgs);
+    case 13: return sizeof(StraitProposeOut);
   }
   return -1;
 }

@@ -1,36 +1,43 @@
-"""Priority-aware dispatch (Algorithm 1) — host mirror of
-infersim/scheduler.py with the reference's names, signatures and error
-behaviour.  The queue/pass bookkeeping is host control flow on the
-reference's own data structures; every prediction, violate/meet check and the
-(latency, gpu_id) argmin run in the CUDA library:
+"""Priority-aware dispatch (Algorithm 1) — the object API of
+infersim/scheduler.py over node records.
 
-* ``PredictivePolicy.propose`` marshals the queue's whole search — every size
-  k in 1..k_max x every GPU x every co-runner — into ONE ``strait_twa`` +
-  ``strait_sweep`` pair (segment = size k), then replays the reference's
-  binary-search probe sequence (scheduler.py:78-90) on the per-size results.
-  best_for is pure, so evaluating sizes the search never probes is harmless.
-* ``check_violate`` / ``check_meet`` are single-pair calls of the same kernels.
+What runs where:
+
+* ``PredictivePolicy.propose`` is ONE ``strait_node_propose`` launch.  The
+  GPUs' records (page-locked, see runtime.py) are read in place by the device,
+  which evaluates every (size, GPU) pair — has_slot, the LP cap, the projection
+  of every running co-runner under its timeline TWA (check_violate), check_meet
+  — then best_for's argmin per size and largest_feasible's probe sequence.  The
+  host writes the candidate's profile rows and reads back one small struct.
+* ``check_violate`` / ``check_meet`` are the same launch for one (size, GPU).
+* ``submit_plan`` / ``complete_batch`` and the AIMD tick mutate records
+  through the library's ``strait_node_*`` entry points (runtime.py).
+* Queues hold the caller's ``Request`` objects (callers mutate them in place,
+  e.g. a deadline), so ``TaskQueue`` / ``early_drop`` stay host control flow.
 """
 from __future__ import annotations
 
-import math
+import ctypes as C
 from collections import deque
 from dataclasses import dataclass
 from typing import Callable, Iterable, Optional, Sequence
 
 import numpy as np
-import torch
 
-from . import _abi
-from . import _device as D
-from . import sweep as SW
+from ._abi import PAIR_MEET, PAIR_VIOLATE, STRAIT_OK, StraitUnavailable, check
+from ._node_abi import ENTRY_BYTES, HDR_BYTES, ProposeArgs, ProposeOut, nlib
 from .domain import Batch, ModelProfile, PriorityLevel, Request, make_batch
-from .predictor import FeedbackSample, InterferencePredictor, UpdateResult, estimate_latency_batch
+from .predictor import FeedbackSample, InterferencePredictor, UpdateResult
 from .runtime import GpuRuntimeState, RunningTaskEntry
 
 
+# ----------------------------------------------------------------------------- queues
+
 class TaskQueue:
-    """FIFO of pending requests for one model (scheduler.py:25-62)."""
+    """Per-model FIFO of pending requests (scheduler.py:25-62).  The queue is
+    schedulable once a full batch waits or its front has aged past the
+    batching timeout.  ``front_generation`` changes whenever a different
+    request becomes the front (the simulator's timeout validity key)."""
 
     def __init__(self, profile: ModelProfile):
         self.profile = profile
@@ -43,53 +50,61 @@ class TaskQueue:
         return len(self.pending)
 
     def push(self, request: Request) -> bool:
+        """Enqueue; True when `request` is now the front."""
+        was_empty = not self.pending
         self.pending.append(request)
-        if len(self.pending) == 1:
-            self.front_generation += 1
-            return True
-        return False
+        self.front_generation += was_empty
+        return was_empty
 
     def front(self) -> Request:
         return self.pending[0]
 
     def timeout_deadline(self) -> float:
-        return self.pending[0].arrival_time + self.profile.batch_timeout_ms
+        return self.front().arrival_time + self.profile.batch_timeout_ms
 
     def eligible(self, now: float) -> bool:
-        if not self.pending:
-            return False
-        return len(self.pending) >= self.profile.max_batch_size or now >= self.timeout_deadline()
+        n = len(self.pending)
+        return n > 0 and (n >= self.profile.max_batch_size or now >= self.timeout_deadline())
 
     def pop_front(self, k: int) -> list[Request]:
-        taken = [self.pending.popleft() for _ in range(k)]
+        q = self.pending
+        taken = [q.popleft() for _ in range(k)]
         self.front_generation += 1
         return taken
 
 
 def early_drop(queue: TaskQueue, now: float) -> list[Request]:
-    """scheduler.py:65-75: drop requests that cannot finish even alone at size 1."""
-    floor_latency = queue.profile.total_latency_ms(1)
-    dropped = [r for r in queue.pending if r.deadline_abs - now < floor_latency]
-    if dropped:
-        old_front = queue.pending[0]
-        queue.pending = deque(r for r in queue.pending if r.deadline_abs - now >= floor_latency)
-        if not queue.pending or queue.pending[0] is not old_front:
+    """scheduler.py:65-75: requests whose remaining slack is below the
+    isolated size-1 latency cannot be served; remove them, keeping the order of
+    the rest.  The front generation moves when the front changes."""
+    floor = queue.profile.total_latency_ms(1)
+    keep, gone = deque(), []
+    for r in queue.pending:
+        slack = r.deadline_abs - now
+        if slack < floor:
+            gone.append(r)
+        elif slack >= floor:  # (a NaN slack is in neither list, as in the reference's two comprehensions)
+            keep.append(r)
+    if gone:
+        head = queue.pending[0]
+        queue.pending = keep
+        if not keep or keep[0] is not head:
             queue.front_generation += 1
-    return dropped
+    return gone
 
 
 def largest_feasible(k_max: int, feasible: Callable[[int], bool]) -> Optional[int]:
-    """scheduler.py:78-90: binary search for the largest feasible size."""
-    lo, hi = 1, k_max
-    best: Optional[int] = None
-    while lo <= hi:
-        mid = (lo + hi) // 2
+    """scheduler.py:78-90: the largest k in 1..k_max with feasible(k), found by
+    bisection (feasibility is monotone); None when k = 1 fails.  The probe
+    sequence is the reference's: mid = (lo + hi) // 2."""
+    found, window = None, (1, k_max)
+    while window[0] <= window[1]:
+        mid = (window[0] + window[1]) // 2
         if feasible(mid):
-            best = mid
-            lo = mid + 1
+            found, window = mid, (mid + 1, window[1])
         else:
-            hi = mid - 1
-    return best
+            window = (window[0], mid - 1)
+    return found
 
 
 @dataclass
@@ -113,120 +128,147 @@ class ScheduleDecision:
     assumed: tuple[float, ...] = ()
 
 
-# ----------------------------------------------------------------------------- snapshot -> SoA
-def _pow2(n: int) -> int:
-    p = 1
-    while p < n:
-        p *= 2
-    return p
+# ----------------------------------------------------------------------------- device propose
+
+def _require_device():
+    try:
+        import torch
+    except ImportError as exc:  # pragma: no cover
+        raise StraitUnavailable("torch is required for the device path") from exc
+    if not torch.cuda.is_available():
+        raise StraitUnavailable("no CUDA device: strait_node_propose has no CPU fallback")
+    return torch
 
 
-def _snapshot(profile: ModelProfile, sizes: Sequence[int], front: float, gpus: Sequence[GpuRuntimeState],
-              now: float, predictor: InterferencePredictor):
-    """Device SoA of segments = sizes, pairs = gpus, triples = co-runners."""
-    nm = len(profile.metrics)
-    G = len(gpus)
-    S = len(sizes)
-    C = min(32, _pow2(max([1] + [len(g.running) for g in gpus])))
-    if any(len(g.running) > 32 for g in gpus):
-        raise ValueError("more than 32 co-runners on one GPU")
-    conc = {g.concurrency_limit for g in gpus}
-    if len(conc) != 1:
-        raise ValueError("all GPUs of a scheduling pass must share one concurrency_limit")
-    a = {
-        "cand_contrib": np.array([profile.throughput_at(k) for k in sizes], dtype=np.float64).T.copy(),
-        "cand_self_cmp": np.array([profile.self_compute_at(k) for k in sizes]),
-        "cand_self_mem": np.array([profile.self_memory_at(k) for k in sizes]),
-        "cand_total": np.array([profile.total_latency_ms(k) for k in sizes]),
-        "cand_kernel": np.array([profile.kernel_latency_ms(k) for k in sizes]),
-        "cand_deadline": np.full(S, profile.deadline_ms),
-        "cand_front": np.full(S, front),
-        "cand_prio": np.full(S, int(profile.priority), dtype=np.int8),
-    }
-    agg = np.array([g.aggregate_throughput for g in gpus], dtype=np.float64).reshape(G, nm)
-    lpa = np.array([g.low_priority_aggregate() for g in gpus], dtype=np.float64).reshape(G, nm)
-    a["gpu_agg"] = np.tile(agg.T, (1, S))
-    a["gpu_lp_agg"] = np.tile(lpa.T, (1, S))
-    a["gpu_cap_pct"] = np.tile(np.array([g.aimd.cap_pct for g in gpus]), S)
-    a["gpu_t_avail"] = np.tile(np.array([g.pcie.t_available for g in gpus]), S)
-    a["gpu_n_running"] = np.tile(np.array([len(g.running) for g in gpus], dtype=np.int8), S)
-    # co-runner slots of one (size-independent) GPU block, then tiled per size
-    T1 = G * C
-    contrib = np.zeros((nm, T1))
-    cmp_ = np.zeros(T1)
-    mem = np.zeros(T1)
-    tk = np.ones(T1)
-    dl = np.zeros(T1)
-    ks = np.zeros(T1)
-    prio = np.zeros(T1, dtype=np.int8)
-    t0 = np.zeros(T1)
-    tl = np.zeros(T1)
-    vl = np.zeros((nm, T1))
-    acc = np.zeros((nm, T1))
-    for gi, g in enumerate(gpus):
-        for j, e in enumerate(g.running):
-            t = gi * C + j
-            contrib[:, t] = e.contribution
-            cmp_[t], mem[t], tk[t], dl[t] = e.self_compute, e.self_memory, e.kernel_latency_ms, e.deadline_abs
-            ks[t] = e.batch.kernel_start if e.kernel_started else e.kernel_start_estimate
-            prio[t] = int(e.priority)
-            tln = e.timeline
-            if not len(tln):
-                raise ValueError("running entry without timeline samples")
-            if now < tln.times[-1]:
-                raise ValueError(f"end_time {now} precedes last sample at {tln.times[-1]}")
-            t0[t], tl[t] = tln.times[0], tln.times[-1]
-            vl[:, t] = tln.values[-1]
-            acc[:, t] = tln.acc
-    # the co-runners' TWA at now on the device (strait_twa, domain.py:249-264)
-    tw = D.empty((nm, T1))
-    keep = [D.dev(x) for x in (t0, tl, vl, acc, np.full(T1, now))]  # alive until the launch is enqueued
-    D.check(D.lib().strait_twa(nm, *[D.ptr(t) for t in keep], T1, D.ptr(tw), D.stream_handle()))
-    dev = {k: D.dev(v, torch.int8 if v.dtype == np.int8 else torch.float64) for k, v in a.items()}
-    rep = lambda x, dt=torch.float64: D.dev(np.tile(x, (1, S)) if x.ndim == 2 else np.tile(x, S), dt)  # noqa: E731
-    dev["ent_contrib"] = rep(contrib)
-    dev["ent_twa"] = tw.repeat(1, S).contiguous()
-    dev["ent_self_cmp"] = rep(cmp_)
-    dev["ent_self_mem"] = rep(mem)
-    dev["ent_t_kernel"] = rep(tk)
-    dev["ent_deadline_abs"] = rep(dl)
-    dev["ent_kstart"] = rep(ks)
-    dev["ent_prio"] = rep(prio, torch.int8)
-    soa = SW.SweepSoA(nm, C, G, conc.pop(), S, float(now), dev)
-    return soa, agg
+class _ProposeBuffers:
+    """Page-locked argument/result blocks of strait_node_propose, grown on
+    demand and reused across calls (the device reads and writes them in place)."""
+
+    def __init__(self):
+        self.cap_g = self.cap_k = 0
+        self.block = None
+
+    def ensure(self, G: int, K: int, nm: int) -> None:
+        if G <= self.cap_g and K <= self.cap_k and self.block is not None:
+            return
+        torch = _require_device()
+        self.cap_g, self.cap_k = max(G, 2 * self.cap_g, 8), max(K, self.cap_k, 8)
+        cg, ck = self.cap_g, self.cap_k
+        sizes = {"recs": 8 * cg, "params": 8 * 16, "cand": 8 * (8 + 4) * ck, "flags": ck * cg,
+                 "lat": 8 * ck * cg, "intf": 8 * ck * cg, "seg_gpu": 4 * ck, "seg_lat": 8 * ck,
+                 "seg_intf": 8 * ck, "out": C.sizeof(ProposeOut)}
+        offs, o = {}, 0
+        for k, n in sizes.items():
+            offs[k] = o
+            o += (n + 63) & ~63
+        self.block = torch.empty(o, dtype=torch.uint8, pin_memory=True)
+        base = self.block.data_ptr()
+        self.addr = {k: base + v for k, v in offs.items()}
+        self.recs = (C.c_uint64 * cg).from_address(self.addr["recs"])
+        self.params = (C.c_double * 16).from_address(self.addr["params"])
+        self.out = ProposeOut.from_address(self.addr["out"])
+        self.np = {
+            "cand": np.frombuffer((C.c_double * (12 * ck)).from_address(self.addr["cand"]), dtype=np.float64),
+            "flags": np.frombuffer((C.c_uint8 * (ck * cg)).from_address(self.addr["flags"]), dtype=np.uint8),
+            "lat": np.frombuffer((C.c_double * (ck * cg)).from_address(self.addr["lat"]), dtype=np.float64),
+            "intf": np.frombuffer((C.c_double * (ck * cg)).from_address(self.addr["intf"]), dtype=np.float64),
+            "seg_gpu": np.frombuffer((C.c_int32 * ck).from_address(self.addr["seg_gpu"]), dtype=np.int32),
+            "seg_lat": np.frombuffer((C.c_double * ck).from_address(self.addr["seg_lat"]), dtype=np.float64),
+            "seg_intf": np.frombuffer((C.c_double * ck).from_address(self.addr["seg_intf"]), dtype=np.float64),
+        }
 
 
-def _sweep_sizes(profile, sizes, front, gpus, now, predictor, use_violate=True, use_meet=True):
-    soa, agg = _snapshot(profile, sizes, front, gpus, now, predictor)
-    P = predictor.params.device_vector()
-    out = SW.alloc_outputs(soa)
-    SW.launch_sweep(soa, P, out, predictor.params.effect_cap, use_violate, use_meet)
-    return {k: D.host(v) for k, v in out.items()}, agg
+_BUFS = _ProposeBuffers()
+_TWA_ERRORS = {1: "no samples", 2: "end_time {now!r} precedes the last timeline sample"}
 
 
-# ----------------------------------------------------------------------------- reference API
+def node_propose(profile: ModelProfile, k_max: int, front_arrival: float, gpus: Sequence[GpuRuntimeState],
+                 now: float, predictor: InterferencePredictor, use_violate: bool = True, use_meet: bool = True,
+                 fixed_size: int = 0, want_pairs: bool = False, stream=None):
+    """One strait_node_propose launch; returns (ProposeOut fields as a dict,
+    per-pair/per-size arrays when `want_pairs`)."""
+    torch = _require_device()
+    nm = len(predictor.params.weights)
+    G, K = len(gpus), k_max
+    for g in gpus:
+        if g.n_metrics != nm:
+            raise ValueError(f"aggregate throughput has {g.n_metrics} metrics, model expects {nm}")
+    if len(profile.throughput[0]) != nm:
+        raise ValueError(f"candidate throughput has {len(profile.throughput[0])} metrics, model expects {nm}")
+    B = _BUFS
+    B.ensure(G, K, nm)
+    for i, g in enumerate(gpus):
+        B.recs[i] = g._rec.dev_addr
+    vec = predictor.params.to_vector()
+    for i, v in enumerate(vec):
+        B.params[i] = v
+    cand = B.np["cand"]
+    rows = np.asarray(profile.throughput[:K], dtype=np.float64)  # [K][nm]
+    cand[:nm * K] = rows.T.reshape(-1)
+    for f, arr in enumerate((profile.self_compute, profile.self_memory, profile.total_latency,
+                             profile.kernel_latency)):
+        cand[(nm + f) * K:(nm + f + 1) * K] = arr[:K]
+    slots = max(g._rec.hdr.slot_cap for g in gpus)
+    stride = (HDR_BYTES + ENTRY_BYTES * slots + 15) & ~15
+    L = nlib()
+    if L.strait_node_propose_smem(K, G, stride) > 200 * 1024:
+        stride = 0  # read the records in place instead of staging them
+    a = ProposeArgs()
+    a.n_metrics, a.n_gpus, a.k_max, a.cand_prio = nm, G, K, int(profile.priority)
+    a.use_violate, a.use_meet, a.fixed_size, a.stage_stride = int(use_violate), int(use_meet), fixed_size, stride
+    a.now, a.effect_cap = now, float(predictor.params.effect_cap)
+    a.deadline_ms, a.front_arrival = profile.deadline_ms, front_arrival
+    ad = B.addr
+    a.params, a.recs, a.out = ad["params"], ad["recs"], ad["out"]
+    a.cand_contrib = ad["cand"]
+    for f, name in enumerate(("cand_self_cmp", "cand_self_mem", "cand_total", "cand_kernel")):
+        setattr(a, name, ad["cand"] + 8 * (nm + f) * K)
+    if want_pairs:
+        a.pair_flags, a.pair_latency, a.pair_intf = ad["flags"], ad["lat"], ad["intf"]
+        a.seg_gpu, a.seg_latency, a.seg_intf = ad["seg_gpu"], ad["seg_lat"], ad["seg_intf"]
+    s = stream if stream is not None else torch.cuda.current_stream()
+    check(L.strait_node_propose(C.byref(a), s.cuda_stream))
+    s.synchronize()
+    o = B.out
+    if o.status != STRAIT_OK:
+        raise ValueError(_TWA_ERRORS.get(o.err_kind, "malformed running entry").format(now=now) +
+                         f" (gpu {gpus[o.err_gpu].gpu_id}, running entry {o.err_pos})")
+    res = {"size": o.size, "gpu_index": o.gpu_index, "latency": o.latency, "intf": o.intf, "probes": o.probes}
+    if not want_pairs:
+        return res, None
+    n = K * G
+    pairs = {"flags": B.np["flags"][:n].reshape(K, G).copy(), "latency": B.np["lat"][:n].reshape(K, G).copy(),
+             "intf": B.np["intf"][:n].reshape(K, G).copy(), "seg_gpu": B.np["seg_gpu"][:K].copy(),
+             "seg_latency": B.np["seg_lat"][:K].copy(), "seg_intf": B.np["seg_intf"][:K].copy()}
+    return res, pairs
+
+
+def _one_pair(gpu: GpuRuntimeState, profile: ModelProfile, size: int, front: float, now: float,
+              predictor: InterferencePredictor, violate: bool):
+    profile._index(size)  # ValueError on a bad size, as the reference's profile accessors
+    _, pairs = node_propose(profile, size, front, [gpu], now, predictor, use_violate=violate, fixed_size=size,
+                            want_pairs=True)
+    return int(pairs["flags"][size - 1, 0]), float(pairs["latency"][size - 1, 0]), float(pairs["intf"][size - 1, 0])
+
+
 def check_violate(gpu: GpuRuntimeState, profile: ModelProfile, size: int, now: float,
                   predictor: InterferencePredictor) -> bool:
-    """scheduler.py:118-161 (one pair of the sweep kernel)."""
-    profile._index(size)  # ValueError on a bad size, as the reference's profile accessors
-    out, _ = _sweep_sizes(profile, [size], 0.0, [gpu], now, predictor)
-    return bool(out["pair_flags"][0] & _abi.PAIR_VIOLATE)
+    """scheduler.py:118-161 — one (size, GPU) pair of strait_node_propose."""
+    flags, _, _ = _one_pair(gpu, profile, size, 0.0, now, predictor, violate=True)
+    return bool(flags & PAIR_VIOLATE)
 
 
 def check_meet(gpu: GpuRuntimeState, profile: ModelProfile, size: int, front_enqueue_time: float, now: float,
                predictor: InterferencePredictor) -> tuple[bool, float, float, tuple[float, ...]]:
-    """scheduler.py:164-185 via strait_estimate_latency."""
-    assumed = tuple(0.5 * a for a in gpu.aggregate_throughput)
-    lat, intf = estimate_latency_batch(predictor.params, [assumed], profile.self_compute_at(size),
-                                       profile.self_memory_at(size), int(profile.priority),
-                                       profile.total_latency_ms(size), profile.kernel_latency_ms(size),
-                                       gpu.pcie.t_available, front_enqueue_time, now)
-    latency, intf = float(lat[0]), float(intf[0])
-    return latency <= profile.deadline_ms, latency, intf, assumed
+    """scheduler.py:164-185 — (ok, latency, intf, assumed) of one pair."""
+    flags, lat, intf = _one_pair(gpu, profile, size, front_enqueue_time, now, predictor, violate=False)
+    return bool(flags & PAIR_MEET), lat, intf, tuple(0.5 * a for a in gpu.aggregate_throughput)
 
+
+# ----------------------------------------------------------------------------- policies
 
 class SchedulingPolicy:
-    """scheduler.py:209-226."""
+    """The pass-level plug-in seam (scheduler.py:209-226)."""
 
     name = "base"
 
@@ -234,19 +276,28 @@ class SchedulingPolicy:
         pass
 
     def queue_order(self, queues: Iterable[TaskQueue], now: float) -> list[TaskQueue]:
-        ready = [q for q in queues if q.pending]
-        ready.sort(key=lambda q: (q.priority.value, q.front().arrival_time, q.model_id))
-        return ready
+        return _ordered(queues, by_priority=True)
 
-    def propose(self, queue: TaskQueue, gpus: Sequence[GpuRuntimeState], now: float):
+    def propose(self, queue: TaskQueue, gpus: Sequence[GpuRuntimeState], now: float) -> Optional[BatchPlan]:
         raise NotImplementedError
 
     def on_hp_violation(self, gpus: Sequence[GpuRuntimeState], gpu_id: Optional[int], now: float) -> None:
         pass
 
 
+def _ordered(queues: Iterable[TaskQueue], by_priority: bool) -> list[TaskQueue]:
+    """Non-empty queues by (priority, front arrival, model id), or without the
+    priority term (the no_priority_scan ablation); stable."""
+    ready = [q for q in queues if q.pending]
+    if by_priority:
+        return sorted(ready, key=lambda q: (q.priority.value, q.front().arrival_time, q.model_id))
+    return sorted(ready, key=lambda q: (q.front().arrival_time, q.model_id))
+
+
 class PredictivePolicy(SchedulingPolicy):
-    """scheduler.py:229-292; one device sweep per propose."""
+    """The interference-predictive policy (scheduler.py:229-292): the largest
+    admitted batch size, on the GPU with the lowest estimated latency — one
+    device launch per propose.  Flags switch mechanisms off for ablations."""
 
     name = "predictive"
 
@@ -259,203 +310,76 @@ class PredictivePolicy(SchedulingPolicy):
         self.launches = 0
 
     def queue_order(self, queues, now):
-        ready = [q for q in queues if q.pending]
-        if self.use_priority_order:
-            ready.sort(key=lambda q: (q.priority.value, q.front().arrival_time, q.model_id))
-        else:
-            ready.sort(key=lambda q: (q.front().arrival_time, q.model_id))
-        return ready
+        return _ordered(queues, by_priority=self.use_priority_order)
 
     def propose(self, queue: TaskQueue, gpus: Sequence[GpuRuntimeState], now: float) -> Optional[BatchPlan]:
-        profile = queue.profile
-        k_max = min(len(queue.pending), profile.max_batch_size)
+        k_max = min(len(queue.pending), queue.profile.max_batch_size)
         if k_max < 1 or not gpus:
             return None
-        ids = [g.gpu_id for g in gpus]
-        order = sorted(range(len(gpus)), key=lambda i: ids[i])  # tie-break on gpu_id
-        gs = [gpus[i] for i in order]
-        sizes = list(range(1, k_max + 1))
-        out, agg = _sweep_sizes(profile, sizes, queue.front().arrival_time, gs, now, self.predictor,
-                                self.use_violate, self.use_meet)
+        res, _ = node_propose(queue.profile, k_max, queue.front().arrival_time, gpus, now, self.predictor,
+                              self.use_violate, self.use_meet)
         self.launches += 1
-        seg_gpu = out["seg_gpu"]
-        k = largest_feasible(k_max, lambda size: seg_gpu[size - 1] >= 0)
-        if k is None:
+        if res["size"] == 0:
             return None
-        g = int(seg_gpu[k - 1])
-        assumed = tuple(0.5 * a for a in gs[g].aggregate_throughput)
-        return BatchPlan(k, gs[g].gpu_id, float(out["seg_latency"][k - 1]), float(out["seg_intf"][k - 1]), assumed)
+        g = gpus[res["gpu_index"]]
+        return BatchPlan(res["size"], g.gpu_id, res["latency"], res["intf"],
+                         tuple(0.5 * a for a in g.aggregate_throughput))
 
     def on_hp_violation(self, gpus, gpu_id, now):
-        if gpu_id is None:
-            for gpu in gpus:
-                gpu.aimd.reset()
-        else:
-            gpus[gpu_id].aimd.reset()
+        for gpu in (gpus if gpu_id is None else [gpus[gpu_id]]):
+            gpu.aimd.reset()
 
+
+# ----------------------------------------------------------------------------- pass driver
 
 def submit_plan(queue: TaskQueue, plan: BatchPlan, gpus: Sequence[GpuRuntimeState], now: float,
                 batch_id: str) -> tuple[Batch, RunningTaskEntry, tuple[float, float]]:
-    """scheduler.py:295-324."""
-    profile = queue.profile
-    requests = queue.pop_front(plan.size)
-    batch = make_batch(batch_id, profile, requests)
-    batch.gpu_id = plan.gpu_id
-    batch.sched_time = now
-    gpu = gpus[plan.gpu_id]
-    t_start, t_end = gpu.pcie.reserve(now, profile.transfer_latency_ms(plan.size))
-    batch.transfer_start = t_start
-    entry = RunningTaskEntry(batch=batch, contribution=profile.throughput_at(plan.size),
-                             self_compute=profile.self_compute_at(plan.size),
-                             self_memory=profile.self_memory_at(plan.size),
-                             kernel_latency_ms=profile.kernel_latency_ms(plan.size),
-                             deadline_abs=requests[0].deadline_abs, intf_predicted=plan.intf_pred,
-                             kernel_start_estimate=t_end)
-    gpu.add_entry(entry, now)
-    return batch, entry, (t_start, t_end)
+    """scheduler.py:295-324: pop the plan's requests into a batch, reserve the
+    GPU's link for its transfer and register it as running — the last two in
+    one library call (GpuRuntimeState.submit_entry)."""
+    prof, k = queue.profile, plan.size
+    requests = queue.pop_front(k)
+    batch = make_batch(batch_id, prof, requests)
+    batch.gpu_id, batch.sched_time = plan.gpu_id, now
+    entry = RunningTaskEntry(batch, prof.throughput_at(k), prof.self_compute_at(k), prof.self_memory_at(k),
+                             prof.kernel_latency_ms(k), requests[0].deadline_abs, plan.intf_pred,
+                             kernel_start_estimate=0.0)
+    window = gpus[plan.gpu_id].submit_entry(entry, prof.transfer_latency_ms(k), now)
+    batch.transfer_start = window[0]
+    return batch, entry, window
 
 
 def complete_batch(gpu: GpuRuntimeState, entry: RunningTaskEntry, measured_kernel_ms: float, now: float,
                    predictor: Optional[InterferencePredictor] = None
                    ) -> tuple[FeedbackSample, Optional[UpdateResult]]:
-    """scheduler.py:327-352; the refit runs in strait_refit."""
+    """scheduler.py:327-352: the feedback sample (TWA of the kernel window,
+    measured / isolated kernel latency), the entry's removal with departure
+    samples on the survivors, then the device refit step."""
+    if not any(e is entry for e in gpu._order):
+        raise RuntimeError(f"gpu {gpu.gpu_id}: batch {entry.batch.batch_id} is not running here")
     twa = entry.timeline.time_weighted_average(now)
-    intf_actual = measured_kernel_ms / entry.kernel_latency_ms
-    sample = FeedbackSample(batch_id=entry.batch.batch_id, colocated_twa=twa, self_compute=entry.self_compute,
-                            self_memory=entry.self_memory, priority=entry.priority, actual=intf_actual,
-                            predicted_at_schedule=entry.intf_predicted)
+    sample = FeedbackSample(entry.batch.batch_id, twa, entry.self_compute, entry.self_memory, entry.priority,
+                            measured_kernel_ms / entry.kernel_latency_ms, entry.intf_predicted)
     gpu.remove_entry(entry, now)
-    result = predictor.update(sample) if predictor is not None else None
-    return sample, result
+    return sample, (None if predictor is None else predictor.update(sample))
 
 
 def run_scheduling_pass(policy: SchedulingPolicy, queues: Iterable[TaskQueue], gpus: Sequence[GpuRuntimeState],
                         now: float, on_submit: Callable[[TaskQueue, BatchPlan], ScheduleDecision],
                         on_drop: Callable[[TaskQueue, list[Request]], None]) -> list[ScheduleDecision]:
-    """scheduler.py:355-378."""
+    """scheduler.py:355-378: queues in policy order; each is early-dropped,
+    then — if still eligible — proposed for and submitted at most once."""
     policy.begin_pass(now)
-    decisions: list[ScheduleDecision] = []
-    for queue in policy.queue_order(queues, now):
-        dropped = early_drop(queue, now)
-        if dropped:
-            on_drop(queue, dropped)
-        if not queue.pending or not queue.eligible(now):
-            continue
-        plan = policy.propose(queue, gpus, now)
-        if plan is None:
-            continue
-        decisions.append(on_submit(queue, plan))
-    return decisions
+    out: list[ScheduleDecision] = []
+    for q in policy.queue_order(queues, now):
+        lost = early_drop(q, now)
+        if lost:
+            on_drop(q, lost)
+        plan = policy.propose(q, gpus, now) if q.eligible(now) else None
+        if plan is not None:
+            out.append(on_submit(q, plan))
+    return out
 
 
-def _isolated_latency_plan(queue: TaskQueue, gpu_id: int, size: int, now: float) -> BatchPlan:
-    """baselines.py:34-37."""
-    latency = (now - queue.front().arrival_time) + queue.profile.total_latency_ms(size)
-    return BatchPlan(size=size, gpu_id=gpu_id, est_latency=latency, intf_pred=1.0, assumed=())
-
-
-class TemporalPolicy(SchedulingPolicy):
-    """baselines.py:40-59: one batch per GPU; largest size meeting the front deadline in isolation."""
-
-    name = "temporal"
-
-    def propose(self, queue, gpus, now):
-        idle = [g for g in gpus if not g.running]
-        if not idle:
-            return None
-        profile = queue.profile
-        deadline = queue.front().deadline_abs
-        k_max = min(len(queue.pending), profile.max_batch_size)
-        size = largest_feasible(k_max, lambda k: now + profile.total_latency_ms(k) <= deadline)
-        return None if size is None else _isolated_latency_plan(queue, idle[0].gpu_id, size, now)
-
-
-class StaticSpatialPolicy(SchedulingPolicy):
-    """baselines.py:62-78: fixed concurrency cap, least-loaded GPU, everything buffered."""
-
-    name = "static"
-
-    def __init__(self, cap: int = 3):
-        self.cap = cap
-
-    def propose(self, queue, gpus, now):
-        open_gpus = [g for g in gpus if len(g.running) < min(self.cap, g.concurrency_limit)]
-        if not open_gpus:
-            return None
-        gpu = min(open_gpus, key=lambda g: (len(g.running), g.gpu_id))
-        return _isolated_latency_plan(queue, gpu.gpu_id, min(len(queue.pending), queue.profile.max_batch_size), now)
-
-
-@dataclass
-class ReactiveState:
-    """baselines.py:81-107."""
-
-    lp_allowance: int = 3
-    default_allowance: int = 3
-    min_allowance: int = 1
-    hp_bound: int = 3
-    reset_period_ms: float = 200.0
-    last_reset: float = 0.0
-
-    def catch_up(self, now: float) -> None:
-        if now - self.last_reset >= self.reset_period_ms:
-            periods = math.floor((now - self.last_reset) / self.reset_period_ms)
-            self.lp_allowance = self.default_allowance
-            self.last_reset += periods * self.reset_period_ms
-
-    def on_hp_violation(self) -> None:
-        self.lp_allowance = max(self.min_allowance, self.lp_allowance - 1)
-
-
-class ReactiveSpatialPolicy(SchedulingPolicy):
-    """baselines.py:110-133: LP concurrency throttled by HP deadline misses."""
-
-    name = "reactive"
-
-    def __init__(self, state: Optional[ReactiveState] = None):
-        self.state = state if state is not None else ReactiveState()
-
-    def begin_pass(self, now: float) -> None:
-        self.state.catch_up(now)
-
-    def _class_open(self, gpu: GpuRuntimeState, priority: PriorityLevel) -> bool:
-        if not gpu.has_slot():
-            return False
-        count = sum(1 for e in gpu.running if e.priority is priority)
-        bound = self.state.lp_allowance if priority is PriorityLevel.LOW else self.state.hp_bound
-        return count < bound
-
-    def propose(self, queue, gpus, now):
-        open_gpus = [g for g in gpus if self._class_open(g, queue.priority)]
-        if not open_gpus:
-            return None
-        gpu = min(open_gpus, key=lambda g: (len(g.running), g.gpu_id))
-        return _isolated_latency_plan(queue, gpu.gpu_id, min(len(queue.pending), queue.profile.max_batch_size), now)
-
-    def on_hp_violation(self, gpus, gpu_id, now):
-        self.state.catch_up(now)
-        self.state.on_hp_violation()
-
-
-POLICY_NAMES = ("predictive", "temporal", "static", "reactive")
-ABLATION_VARIANTS = ("full", "no_priority_scan", "no_gamma_advantage", "no_meet", "no_violate_aimd")
-
-
-def make_policy(name: str, predictor: Optional[InterferencePredictor] = None, variant: str = "full"):
-    """baselines.py:136-160 registry.  Whole replays of every policy run on the
-    device (simulation.run / replay.ReplayBatch); these objects serve the
-    per-call pass API (run_scheduling_pass)."""
-    if name == "predictive":
-        if variant not in ABLATION_VARIANTS:
-            raise ValueError(f"unknown ablation variant {variant!r}")
-        if predictor is None:
-            raise ValueError("predictive policy needs a predictor")
-        return PredictivePolicy(predictor, use_priority_order=variant != "no_priority_scan",
-                                use_meet=variant != "no_meet", use_violate=variant != "no_violate_aimd")
-    if name == "temporal":
-        return TemporalPolicy()
-    if name == "static":
-        return StaticSpatialPolicy()
-    if name == "reactive":
-        return ReactiveSpatialPolicy()
-    raise ValueError(f"unknown policy {name!r}, expected one of {POLICY_NAMES}")
+from .baselines import (ABLATION_VARIANTS, POLICY_NAMES, ReactiveSpatialPolicy, ReactiveState,  # noqa: E402,F401
+                        StaticSpatialPolicy, TemporalPolicy, make_policy)

@@ -39,11 +39,12 @@ def test_ctypes_mirrors_match_the_header_structs():
     its C struct (strait_struct_size), so no field is misplaced."""
     import ctypes as C
 
-    from paper_2604_28175_b200 import _abi, _replay_abi as R, devgen, ground_truth
+    from paper_2604_28175_b200 import _abi, _node_abi as N, _replay_abi as R, devgen, ground_truth
 
     lib = _abi.lib()
     mirrors = [_abi.SweepArgs, _abi.SweepExpandArgs, _abi.RefitArgs, R.ReplayModels, R.ReplayConfig,
-               R.ReplayArgs, None, R.MetricsArgs, devgen.StreamSpec, ground_truth.GroundTruth]
+               R.ReplayArgs, None, R.MetricsArgs, devgen.StreamSpec, ground_truth.GroundTruth, N.GpuHdr,
+               N.NodeEntry, N.ProposeArgs, N.ProposeOut]
     for i, m in enumerate(mirrors):
         want = lib.strait_struct_size(i)
         got = R.TRACE_DTYPE.itemsize if m is None else C.sizeof(m)
