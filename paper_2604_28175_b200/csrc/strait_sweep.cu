@@ -157,8 +157,15 @@ __device__ __forceinline__ void tile_compute(const StraitSweepArgs& a, const Til
   // ---- 1. triple: projection of one running entry (scheduler.py:137-160) ----
   const int nrun = active ? nrun_s[pl] : 0;
   const int cprio = active ? cprio_s[sl] : 0;
+  // the LOW candidate's AIMD-cap test answers check_violate before any co-runner is read (scheduler.py:129-135)
+  bool capv = false;
+  if (active && cprio == 1) {
+    const double cap_fraction = pair[(2 * NM) * TP + pl] / 100.0;
+#pragma unroll
+    for (int m = 0; m < NM; ++m) capv |= pair[(NM + m) * TP + pl] + cand[m * spb + sl] > cap_fraction;
+  }
   bool viol = false;
-  if (active && c < nrun && e.prio <= cprio) {
+  if (active && c < nrun && e.prio <= cprio && !capv) {
     // current progress under the time-weighted co-location (R6 input)
     const double intf_cur = pr.predict(e.tw, e.cmp, e.mem, e.prio);
     const double elapsed = py_max(0.0, now - e.ks);
@@ -537,8 +544,16 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
     const int nrun = active ? ((const int8_t*)(stage + L.nrun))[pl] : 0;
     const int cprio = active ? ((const int8_t*)(stage + L.cprio))[4 * sl + (int)((tile * spb + sl) & 3)] : 0;
     const int eprio = active ? ((const int8_t*)(stage + L.eprio))[local] : 0;
+    // check_violate answers True at the LOW candidate's AIMD-cap test before it
+    // reads any co-runner (scheduler.py:129-135): such pairs project nothing
+    bool capv = false;
+    if (active && cprio == 1) {
+      const double cap_fraction = pair[(2 * NM) * TP + pl] / 100.0;
+#pragma unroll
+      for (int m = 0; m < NM; ++m) capv |= pair[(NM + m) * TP + pl] + cand[m * spb + sl] > cap_fraction;
+    }
     bool viol = false;
-    if (active && c < nrun && eprio <= cprio && !(diag & 8)) {  // diag 8: skip the projections (timing only)
+    if (active && c < nrun && eprio <= cprio && !capv && !(diag & 8)) {  // diag 8: skip the projections (timing only)
       double tw[NM], nagg[NM];
 #pragma unroll
       for (int m = 0; m < NM; ++m) tw[m] = ent[(NM + m) * TT + local];

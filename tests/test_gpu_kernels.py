@@ -1,8 +1,8 @@
 """GPU parity: the CUDA kernels (through the C-ABI) against the reference's
-golden vectors and the C oracle.  Decisions/flags must be identical; floats
-within 1e-5 relative (north_star), and we additionally require that the
-overwhelming majority are bit-identical (libdevice exp/log differ from glibc
-by <= 1 ulp on a small fraction of inputs)."""
+golden vectors and the C oracle.  Decisions/flags must be identical, and so
+must every float: the device exp/log/pow are restatements of the reference
+host's glibc routines (csrc/strait_libm.cuh), so the north_star's 1e-5
+relative bound is checked but bit-identity is what is required."""
 import ctypes as C
 import os
 
@@ -14,16 +14,17 @@ from conftest import sweep_case
 
 pytestmark = pytest.mark.gpu
 
-REL = 1e-5
+REL = 1e-5  # north_star tolerance for float latency predictions
 
 
-def assert_close_bits(got, want, rel=REL, min_exact=0.9, what=""):
+def assert_close_bits(got, want, rel=REL, what=""):
+    """Within `rel` (north_star) AND bit-identical, NaNs matching."""
     got, want = np.asarray(got), np.asarray(want)
     both_nan = np.isnan(got) & np.isnan(want)
     ok = both_nan | (got == want) | (np.abs(got - want) <= rel * np.maximum(np.abs(want), 1e-300))
     assert ok.all(), f"{what}: {np.count_nonzero(~ok)} values beyond {rel} rel"
-    exact = (both_nan | (got == want)).mean() if got.size else 1.0
-    assert exact >= min_exact, f"{what}: only {exact:.4%} bit-identical"
+    exact = both_nan | (got == want)
+    assert exact.all(), f"{what}: {np.count_nonzero(~exact)} of {got.size} values not bit-identical"
 
 
 def test_predict_vs_golden(cuda, golden):
@@ -53,8 +54,6 @@ def test_estimate_latency_vs_golden(cuda, golden):
     for i in range(len(g["latency"])):
         p = PredictorParams(weights=(0.0,) * 5)
         p.apply_vector(list(g["params"][i]))
-        if i >= 400:
-            break
         lat, _ = estimate_latency_batch(p, [g["assumed"][i]], g["cmp"][i], g["mem"][i], g["prio"][i], g["total"][i],
                                         g["kernel"][i], g["t_avail"][i], g["front"][i], g["now"][i])
         got.append(lat[0])
@@ -89,11 +88,10 @@ def test_refit_vs_golden(cuda, golden, stream):
     traj = g[f"{stream}_traj"]
     got_state = np.array(pred.params.to_vector() + pred.opt.m + pred.opt.v)
     assert pred.opt.step == traj[-1, -1]
-    assert_close_bits(got_state, traj[-1, :-1], rel=1e-9, min_exact=0.0, what="final state")
+    assert_close_bits(got_state, traj[-1, :-1], what="final state")
     np.testing.assert_array_equal([r.skipped for r in res], g[f"{stream}_skipped"])
     np.testing.assert_array_equal([r.saturated for r in res], g[f"{stream}_saturated"])
-    assert_close_bits([r.predicted for r in res], g[f"{stream}_predicted"], rel=1e-9, min_exact=0.0,
-                      what="predicted")
+    assert_close_bits([r.predicted for r in res], g[f"{stream}_predicted"], what="predicted")
 
 
 def _golden_sweep_check(golden, case, pname, vname, uv, um, path):
@@ -181,7 +179,7 @@ def test_round_equals_sweep_plus_refit(cuda, oracle):
     assert torch.equal(state, state2) and torch.equal(step, step2)
     # and the refit agrees with the oracle chain
     ostate, ostep, _, _, _ = oracle.refit(pred.params.to_vector() + pred.opt.m + pred.opt.v, 0, fb, nm=5)
-    assert_close_bits(D.host(state2), ostate, rel=1e-9, min_exact=0.0, what="round refit")
+    assert_close_bits(D.host(state2), ostate, what="round refit")
     assert int(D.host(step2)[0]) == ostep
 
 
