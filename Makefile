@@ -47,7 +47,17 @@ build/prof/%.o: $(CDIR)/%.cu $(COMMON_HDR) $(REPLAY_HDR)
 $(PROF_LIB): $(PROF_OBJS)
 	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(PROF_OBJS)
 
+# diagnostic: the sweep with its STRAIT_SWEEP_DIAG timing switches compiled in (scripts/gpu_diag2.sh)
+DIAG_LIB := build/diag/_strait.so
+DIAG_OBJS := $(patsubst $(CDIR)/%.cu,build/diag/%.o,$(CSRC))
+diag: $(DIAG_LIB)
+build/diag/%.o: $(CDIR)/%.cu $(COMMON_HDR) $(REPLAY_HDR) $(SWEEP_HDR)
+	@mkdir -p build/diag
+	$(NVCC) $(NVFLAGS) -DSTRAIT_SWEEP_DIAG_BUILD=1 -dc -o $@ $<
+$(DIAG_LIB): $(DIAG_OBJS)
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(DIAG_OBJS)
+
 clean:
 	rm -rf build $(LIB) oracle/build
 
-.PHONY: all oracle clean prof
+.PHONY: all oracle clean prof diag

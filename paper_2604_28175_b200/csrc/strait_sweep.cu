@@ -592,34 +592,54 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
     asm volatile("bar.sync %0, %1;" ::"r"(bar1), "r"(8 * 32) : "memory");
 
     // ---- 2. pair: LP cap + check_meet, one lane per pair on the first ceil(TP/32) warps ----
+    // The pair lanes first copy what they still need out of the stage into
+    // registers and release it, so the producer refills it while the meet
+    // predictions and the argmin run (they only touch the stage's result area,
+    // which TMA never writes and which only these warps use, in tile order).
     {
       const int pp = wg * 32 + lane;
-      if (pp < TP) {
-        const int psl = pp / G;
-        const int pn = ((const int8_t*)(stage + L.nrun))[pp];
-        const int pprio = ((const int8_t*)(stage + L.cprio))[4 * psl + (int)((tile * spb + psl) & 3)];
+      const bool pact = pp < TP;
+      const int psl = pact ? pp / G : 0;
+      int pn = 0, pprio = 0;
+      bool violate = false;
+      double agg[NM], cmp = 0.0, mem = 0.0, total = 0.0, kern = 0.0, front = 0.0, dline = 0.0, tav = 0.0;
+      if (pact) {
+        pn = ((const int8_t*)(stage + L.nrun))[pp];
+        pprio = ((const int8_t*)(stage + L.cprio))[4 * psl + (int)((tile * spb + psl) & 3)];
+        violate = s_viol[pp] != 0;
+        if (pprio == 1) {  // LOW candidate vs the AIMD cap (scheduler.py:130-135)
+          const double cap_fraction = pair[(2 * NM) * TP + pp] / 100.0;  // runtime.py:39-40
+#pragma unroll
+          for (int m = 0; m < NM; ++m)
+            if (pair[(NM + m) * TP + pp] + cand[m * spb + psl] > cap_fraction) violate = true;
+        }
+#pragma unroll
+        for (int m = 0; m < NM; ++m) agg[m] = pair[m * TP + pp];
+        tav = pair[(2 * NM + 1) * TP + pp];
+        cmp = cand[(NM + 0) * spb + psl];
+        mem = cand[(NM + 1) * spb + psl];
+        total = cand[(NM + 2) * spb + psl];
+        kern = cand[(NM + 3) * spb + psl];
+        front = cand[(NM + 4) * spb + psl];
+        dline = cand[(NM + 5) * spb + psl];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);  // the TMA region of this stage is free
+      if (pact) {
         uint8_t flags = 0;
         double lat = nan, intf = nan;
         bool admitted = false;
         if (pn < a.concurrency_limit) {  // has_slot (runtime.py:101-102)
           flags |= STRAIT_PAIR_HAS_SLOT;
-          bool violate = s_viol[pp] != 0;
-          if (pprio == 1) {  // LOW candidate vs the AIMD cap (scheduler.py:130-135)
-            const double cap_fraction = pair[(2 * NM) * TP + pp] / 100.0;  // runtime.py:39-40
-#pragma unroll
-            for (int m = 0; m < NM; ++m)
-              if (pair[(NM + m) * TP + pp] + cand[m * spb + psl] > cap_fraction) violate = true;
-          }
           if (violate) flags |= STRAIT_PAIR_VIOLATE;
           double assumed[NM];  // check_meet: half the GPU aggregate (scheduler.py:178)
 #pragma unroll
-          for (int m = 0; m < NM; ++m) assumed[m] = 0.5 * pair[m * TP + pp];
+          for (int m = 0; m < NM; ++m) assumed[m] = 0.5 * agg[m];
           intf = (diag & 16) ? assumed[0]  // diag 16: skip check_meet's prediction (timing only)
-                             : pr.predict(assumed, cand[(NM + 0) * spb + psl], cand[(NM + 1) * spb + psl], pprio);
-          const double wait = py_max(0.0, pair[(2 * NM + 1) * TP + pp] - now);  // pcie.py:21-23
-          lat = cand[(NM + 2) * spb + psl] + wait + (intf - 1.0) * cand[(NM + 3) * spb + psl] +
-                (now - cand[(NM + 4) * spb + psl]);
-          const bool ok = lat <= cand[(NM + 5) * spb + psl];
+                             : pr.predict(assumed, cmp, mem, pprio);
+          const double wait = py_max(0.0, tav - now);  // pcie.py:21-23
+          lat = total + wait + (intf - 1.0) * kern + (now - front);
+          const bool ok = lat <= dline;
           if (ok) flags |= STRAIT_PAIR_MEET;
           admitted = !(a.use_violate && violate) && !(a.use_meet && !ok);
           if (admitted) flags |= STRAIT_PAIR_FEASIBLE;
@@ -662,8 +682,9 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
         }
       }
     }
+    // (the stage was released before the meet predictions; the result area is
+    // next written by these same warps, for tile + nstages, in program order)
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
   }
 }
 
