@@ -87,6 +87,25 @@ def loaded_repo_libs() -> list[str]:
     return sorted(out)
 
 
+def sweep_sass_sha256() -> str | None:
+    """SHA-256 of the headline kernel's SASS (ties a stored ncu capture to the timed build)."""
+    import hashlib
+    import subprocess
+
+    from paper_2604_28175_b200 import _abi
+
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", "-fun", SWEEP_KERNEL, _abi.LIB_PATH], capture_output=True,
+                             text=True, timeout=60).stdout
+    except (OSError, subprocess.SubprocessError):
+        return None
+    body = "\n".join(line for line in out.splitlines() if line.strip().startswith("/*"))
+    return hashlib.sha256(body.encode()).hexdigest() if body else None
+
+
+SWEEP_KERNEL = "_ZN6strait15sweep_ws_kernelILi5ELi4ELi64EEEv15StraitSweepArgs15StraitRefitArgsiiii14CUtensorMap_stS3_i"
+
+
 def host_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -380,8 +399,9 @@ def reduce_max_sum(dist, ws, maxes, sums):
 
     if ws == 1:
         return list(maxes), list(sums)
-    mx = torch.tensor(maxes, dtype=torch.float64, device="cuda")
-    sm = torch.tensor(sums, dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    mx = torch.tensor(maxes, dtype=torch.float64, device=dev)
+    sm = torch.tensor(sums, dtype=torch.float64, device=dev)
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     dist.all_reduce(sm, op=dist.ReduceOp.SUM)
     return mx.tolist(), sm.tolist()
@@ -392,7 +412,7 @@ def reduce_all_ok(dist, ws, ok: bool) -> bool:
 
     if ws == 1:
         return ok
-    v = torch.tensor([0.0 if ok else 1.0], device="cuda")
+    v = torch.tensor([0.0 if ok else 1.0], device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(v, op=dist.ReduceOp.SUM)
     return v.item() == 0
 
@@ -730,14 +750,20 @@ def run_ours(args):
     if os.path.exists(peaks_path):
         peak, peak_src = float(json.load(open(peaks_path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     kern_ms = weak["kern_ms"]
-    achieved = weak["alg_bytes"] / (kern_ms / 1e3) / 1e9
+    # achieved bandwidth on SURVEY §8(d)'s algorithmic bytes (89 B/triple with the 8-B intf_cur,
+    # 114 B/pair, 101 B/segment = 117.9 B/triple); the kernel's own record (twa[5] instead of
+    # intf_cur) moves 121 B/triple and is reported beside it
     survey_bytes = 89 * weak["triples"] + 114 * (weak["triples"] // 4) + 101 * (weak["triples"] // 256)
-    traffic, traffic_src = None, None
+    achieved = survey_bytes / (kern_ms / 1e3) / 1e9
+    record_gbs = weak["alg_bytes"] / (kern_ms / 1e3) / 1e9
+    traffic, traffic_src, traffic_match = None, None, None
     tfile = os.path.join(REPO, "profiles", "sweep_traffic.json")
     if os.path.exists(tfile):
         t = json.load(open(tfile))
         traffic = t.get("dram_bytes_per_launch")
-        traffic_src = f"stored ncu --set full capture ({t.get('source', 'profiles/')}), not measured in this run"
+        traffic_match = t.get("sass_sha256") == sweep_sass_sha256()
+        traffic_src = (f"stored ncu --set full capture ({t.get('source', 'profiles/')}); SASS of the capture "
+                       f"{'==' if traffic_match else '!='} the kernel timed here")
     parity = {"c3_round0": weak.get("parity", {}).get("ok") if "parity" in weak else None}
     parity["c3_round0"] = c3_ok if "parity" in weak else None
     for k, v in legs.items():
@@ -755,13 +781,15 @@ def run_ours(args):
                         "tables) -> H2D -> strait_sweep_expand -> strait_round (C-ABI) -> D2H decisions; "
                         f"{args.e2e_steps} steps pipelined over copy/compute/D2H streams, total / steps"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
-                     "kernel": f"strait_round ({weak['path']} sweep path)",
-                     "algorithmic_bytes_per_launch": weak["alg_bytes"],
-                     "bytes_basis": "121 B/triple + 114 B/pair + 109 B/segment: the triple record carries twa[5] "
-                                    "(40 B), because intf_cur depends on the round's refit params (DESIGN.md 3.1)",
-                     "frac_survey_basis": survey_bytes / (kern_ms / 1e3) / 1e9 / peak,
-                     "survey_bytes_per_launch": survey_bytes, "kernel_ms": kern_ms},
+                     "traffic": traffic, "traffic_source": traffic_src, "traffic_matches_kernel": traffic_match,
+                     "peak_source": peak_src, "kernel": f"strait_round ({weak['path']} sweep path)",
+                     "bytes_basis": "SURVEY §8(d): 89 B/triple + 114 B/pair + 101 B/segment (117.9 B/triple)",
+                     "algorithmic_bytes_per_launch": survey_bytes, "kernel_ms": kern_ms,
+                     "record_basis": {"bytes_per_launch": weak["alg_bytes"], "achieved_gbs": record_gbs,
+                                      "frac": record_gbs / peak,
+                                      "note": "121 B/triple + 114 B/pair + 109 B/segment: the record carries "
+                                              "twa[5] (40 B) because intf_cur depends on the round's refit "
+                                              "parameters (DESIGN.md 3.1)"}},
         "gpu_launches": int(weak["launches"]),
         "clocks": weak["clocks"],
         "parity": parity,
