@@ -25,6 +25,12 @@ int sm_count() {
 
 namespace strait {
 namespace rp {
+bool replay_cta_enabled(bool wide) {
+  const char* e = getenv("STRAIT_REPLAY_NW");
+  if (e && atoi(e) == 1) return false;
+  if (e && atoi(e) > 1) return true;
+  return wide;
+}
 int replay_occupancy(int64_t n_replays, int wpc) {
   if (const char* e = getenv("STRAIT_REPLAY_OCC")) return atoi(e) >= 4 ? 4 : 1;
   return n_replays > (int64_t)sm_count() * 2 * wpc ? 4 : 1;
@@ -85,8 +91,13 @@ extern "C" int strait_replay(const StraitReplayArgs* a, void* stream) {
   // SM), then one warp per CTA so the hardware spreads the (heaviest-first ordered)
   // replays over SMs and sub-partitions; past that, the 16-replays-per-SM kernel
   // a traced launch (event log) always runs the latency variant with the log compiled in
-  const int minb = a->trace ? 0 : replay_occupancy(a->n_replays, wpc);
+  int minb = a->trace ? 0 : replay_occupancy(a->n_replays, wpc);
   if (minb < 4) wpc = 1;
+  // at most one replay per SM and more running-batch slots than a warp has lanes (C5's 64 GPUs):
+  // a CTA of kCtaWarps warps per replay (STRAIT_REPLAY_NW=8 forces it, =1 disables it)
+  if (minb == 1 && a->n_replays <= (int64_t)sm_count() && cta_replay_smem(*a) &&
+      replay_cta_enabled((int64_t)a->max_gpus * a->max_concurrency > 32))
+    minb = 2;
   cudaStream_t st = (cudaStream_t)stream;
   int rc = STRAIT_EINVAL;
   switch (md.n_metrics) {

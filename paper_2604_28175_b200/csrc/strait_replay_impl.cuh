@@ -61,7 +61,7 @@ namespace rp {
 enum { RPF_SELECT, RPF_ARRIVAL, RPF_RANK, RPF_DROP, RPF_ELIG, RPF_PROPOSE, RPF_SUBMIT, RPF_ICUR, RPF_TIMEOUTS,
        RPF_TC, RPF_KC_PRE, RPF_KC_UPDATE, RPF_KC_POST, RPF_TICK, RPF_POST, RPF_TOTAL,
        RPF_N_QUEUES, RPF_N_ELIGIBLE, RPF_N_PROPOSE_WIDE, RPF_N_SUBMIT, RPF_N_ICUR_ALL, RPF_SUM_KMAX, RPF_N_NOSLOT,
-       RPF_SUM_ENTRIES, RPF_N };
+       RPF_SUM_ENTRIES, RPF_CTA_A, RPF_CTA_B, RPF_CTA_M, RPF_N_CTA, RPF_N };
 #define RP_CNT(i) (++prof[i])
 extern __device__ unsigned long long g_replay_prof[RPF_N];
 #define RP_T(v) const long long v = clock64()
@@ -116,16 +116,37 @@ enum { SD_DL, SD_KS, SD_T0, SD_TL, SD_REM, SD_SLOW, SD_NOISE, SD_LAST, SD_WORK, 
        SD_TK, SD_VL };
 enum { SI_BID, SI_REQ0, SI_GPU, SI_J, SI_N };  // SI_GPU / SI_J: s % G and s / G, precomputed
 enum { SB_MODEL, SB_SIZE, SB_PRIO, SB_STARTED, SB_LIVE, SB_TLEN, SB_N };
-enum { GD_TAV, GD_CAP, GD_TICK, GD_AGG };  // then NM aggregates, NM LP aggregates, C pending reservations
+// GD_CAPF = cap_fraction() = cap_pct / 100 (runtime.py:39-40), refreshed wherever the cap changes
+enum { GD_TAV, GD_CAP, GD_TICK, GD_CAPF, GD_AGG };  // then NM aggregates, NM LP aggregates, C pending reservations
 enum { GI_NRUN, GI_PHEAD, GI_PN, GI_N };
 enum { QI_HEAD, QI_TAIL, QI_FGEN, QI_TGEN, QI_EGEN, QI_ORD, QI_N };
+
+// Job block of a CTA-per-replay launch (NW > 1 warps per replay, below): the
+// master warp posts one of these, the helper warps read it after barrier 1.
+enum { JOB_EXIT, JOB_ICUR, JOB_PROPOSE, JOB_SELECT };
+struct Job {
+  int kind, m, kmax, cprio, k0, pad;
+  double now, dl, front;
+};
+// one warp's partial of a reduction: an event-home minimum, or a size's best GPU
+struct Part {
+  double t, x;
+  unsigned long long key;
+  int g, pad;
+};
 
 struct Layout {
   int G, C, M, NM, S, NE;
   size_t P, sd, gd, ed, ek, qd, qf, sl, si, gi, qi, sb, go, qb, bytes;
+  // CTA-per-replay scratch (nw > 1 only): job, per-(size, GPU, co-runner) violate
+  // bits, per-(size, GPU) meet results, per-warp reduction partials
+  size_t jb, pv, plat, pintf, pm, part;
   __host__ __device__ static int sd_fields(int nm) { return SD_VL + 4 * nm; }
   __host__ __device__ static int gd_fields(int nm, int c) { return GD_AGG + 2 * nm + c; }
-  __host__ __device__ Layout(int g, int c, int m, int nm) : G(g), C(c), M(m), NM(nm) {
+  // items of the CTA propose: sizes (<= 32) x GPUs x (co-runner slots + the meet)
+  __host__ __device__ static int cta_sizes(int b) { return b < 32 ? b : 32; }
+  __host__ __device__ static int cta_chunks(int g) { return g <= 32 ? 1 : (g + 31) / 32; }
+  __host__ __device__ Layout(int g, int c, int m, int nm, int nw = 1, int b = 0) : G(g), C(c), M(m), NM(nm) {
     S = G * C;
     NE = S + M + 2;
     size_t o = 0;
@@ -134,7 +155,7 @@ struct Layout {
       o = al(o + n);
       return r;
     };
-    P = take(8 * (NM + 7));
+    P = take(8 * (NM + 8));  // params, then log(base) for the helper warps
     sd = take(8 * (size_t)sd_fields(NM) * S);
     gd = take(8 * (size_t)gd_fields(NM, C) * G);
     ed = take(8 * (size_t)NE);
@@ -148,6 +169,17 @@ struct Layout {
     sb = take((size_t)SB_N * S);
     go = take((size_t)C * G);
     qb = take((size_t)M);
+    jb = pv = plat = pintf = pm = part = 0;
+    if (nw > 1) {
+      const size_t kg = (size_t)cta_sizes(b) * G;
+      jb = take(sizeof(Job));
+      pv = take(kg * (C + 1));
+      plat = take(8 * kg);
+      pintf = take(8 * kg);
+      pm = take(kg);
+      const size_t np = (size_t)cta_sizes(b) * cta_chunks(G);
+      part = take(sizeof(Part) * (np > (size_t)nw ? np : (size_t)nw));
+    }
     bytes = o;
   }
 };
@@ -198,7 +230,15 @@ struct Geom<3> {
   }
 };
 
-template <int NM, typename MathT, bool TR, bool LEAN, int GEOM>
+// NW = warps per replay.  NW = 1: one warp runs the whole replay.  NW > 1 (one
+// replay per CTA, for single replays and few-replay launches): warp 0 (the
+// master) runs the event loop exactly as with NW = 1; at the wide steps —
+// intf_cur of every running entry, a propose's (size, GPU, co-runner)
+// projections, and the next-event scan over many homes — it posts a Job and
+// the NW - 1 helper warps, parked on named barrier 1, join it.  Every job reads
+// the replay state and writes only per-item scratch (or per-slot caches that
+// no other item touches); barrier 2 ends it.  Same arithmetic, same bits.
+template <int NM, typename MathT, bool TR, bool LEAN, int GEOM, int NW = 1>
 struct Sim : Geom<GEOM> {
   using Geom<GEOM>::G;
   using Geom<GEOM>::C;
@@ -214,10 +254,18 @@ struct Sim : Geom<GEOM> {
   static constexpr int SD_AEX = SD_VL + 3 * NM;  // aggregate_excluding(entry) as last stamped
   static constexpr int GD_LPA = GD_AGG + NM;     // low_priority_aggregate()
   static constexpr int GD_PEND = GD_AGG + 2 * NM;
+  static constexpr bool CTA = NW > 1;
+  static constexpr int NT = NW * 32;
   // ---- launch-wide inputs
   const StraitReplayArgs* A;
   const StraitReplayConfig* cf;
   int lane;
+  int w;  // warp of the replay's CTA (0 = master); 0 when NW = 1
+  // CTA scratch (Layout::jb ...)
+  Job* jb;
+  uint8_t *pv, *pm;
+  double *plat, *pintf;
+  Part* part;
   int64_t r, base, N;     // request range [base, base + N)
   // ---- shared-memory state: grouped field arrays of this warp's slice
   double *P, *sd, *gd, *ed, *qd;
@@ -253,6 +301,39 @@ struct Sim : Geom<GEOM> {
   __device__ __forceinline__ int slot_at(int g, int p) const { return slot(g, ORD(p, g)); }
 
   __device__ __forceinline__ void sync() const { __syncwarp(); }
+  // named barrier over the replay's NW warps (ids 1-3; 0 is __syncthreads)
+  __device__ __forceinline__ void cta_bar(int id) const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NT) : "memory");
+  }
+  // master: the job fields were written by lane 0; wake the helpers
+  __device__ __forceinline__ void post_job() const {
+    __syncwarp();
+    cta_bar(1);
+  }
+  // helpers: the predictor as the master holds it (P + log(base) in shared memory)
+  __device__ __forceinline__ void load_shared_pred() {
+    pr.scale = P[0];
+    pr.log_base = P[NP];
+    pr.offset = P[2];
+#pragma unroll
+    for (int i = 0; i < NM; ++i) pr.w[i] = P[3 + i];
+    pr.w_cmp = P[3 + NM];
+    pr.w_mem = P[4 + NM];
+    pr.coeff[0] = P[5 + NM];
+    pr.coeff[1] = P[6 + NM];
+    pr.cap = cf->effect_cap;
+#if STRAIT_LIBM
+    pr.etab = glibc::exp_table();
+#endif
+  }
+  // master: (re)load the predictor from P and publish log(base) to the helpers
+  __device__ __forceinline__ void load_pred() {
+    pr.load(P, cf->effect_cap);
+    if constexpr (CTA) {
+      if (lane == 0) P[NP] = pr.log_base;
+      __syncwarp();
+    }
+  }
   // Uniform scalar store: every lane computed v; lane 0 writes it after the warp
   // has finished its earlier reads of shared state (write-after-read).  Readers
   // of the new value come after a sync() (read-after-write).
@@ -509,6 +590,7 @@ struct Sim : Geom<GEOM> {
         const double old = GD(GD_CAP, g);
         cap = cf->aimd_floor;
         GD(GD_CAP, g) = cap;
+        GD(GD_CAPF, g) = MathT::div(cap, 100.0);
         changed = cap != old;
       }
       const unsigned mask = __ballot_sync(kFull, changed);
@@ -588,7 +670,7 @@ struct Sim : Geom<GEOM> {
     sync();
     if (owner) P[lane] = p;
     sync();
-    pr.load(P, cap);
+    load_pred();
   }
 
   // ------------------------------------------------------------ dispatch (scheduler.py)
@@ -617,6 +699,17 @@ struct Sim : Geom<GEOM> {
   // (has_slot is tested first), so only their entries are evaluated: the
   // slots are compacted into a list and processed 32 at a time
   __device__ __forceinline__ void icur_all(double now) const {
+    if constexpr (CTA) {
+      if (S > 32) {  // one slot per thread of the CTA
+        if (lane == 0) {
+          jb->kind = JOB_ICUR;
+          jb->now = now;
+        }
+        post_job();
+        job_icur(now);
+        return;
+      }
+    }
     int count = 0;
     for (int s0 = 0; s0 < S; s0 += 32) {
       const int s = s0 + lane;
@@ -632,6 +725,12 @@ struct Sim : Geom<GEOM> {
   __device__ __forceinline__ void icur_gpu(int g, double now) const {
     if (lane < GI(GI_NRUN, g)) icur_slot(slot_at(g, lane), now);
     __syncwarp();
+  }
+  // JOB_ICUR (every warp of the CTA): intf_cur of the entries whose GPU has a free slot
+  __device__ __forceinline__ void job_icur(double now) const {
+    for (int s = w * 32 + lane; s < S; s += NT)
+      if (SB(SB_LIVE, s) && GI(GI_NRUN, SI(SI_GPU, s)) < CONC) icur_slot(s, now);
+    cta_bar(2);
   }
 
   // the candidate batch (model m at size k): profile row at k (domain.py:52-105)
@@ -651,7 +750,7 @@ struct Sim : Geom<GEOM> {
   // check_violate (scheduler.py:118-161) of the candidate on GPU g; lane-local.
   __device__ __forceinline__ bool violate(int g, const Cand& cd, int cprio, double now) const {
     if (cprio == 1) {  // LOW: LP aggregate + contribution vs the AIMD cap (:130-135)
-      const double capf = MathT::div(GD(GD_CAP, g), 100.0);
+      const double capf = GD(GD_CAPF, g);
 #pragma unroll
       for (int i = 0; i < NM; ++i)
         if (GD(GD_LPA + i, g) + cd.c[i] > capf) return true;
@@ -783,6 +882,181 @@ struct Sim : Geom<GEOM> {
     return size;
   }
 
+  // JOB_PROPOSE (every warp of the CTA): PredictivePolicy.propose's whole
+  // (size x GPU x co-runner) search for queue m.
+  //  A. items (k, g, c): c < CONC is check_violate's projection of running entry
+  //     c of GPU g (scheduler.py:137-160), c == CONC the pair's LP-cap test
+  //     (:130-135) and check_meet (:164-185) — independent chains, one per thread;
+  //  B. pairs (k, g): has_slot, the OR of the pair's projections, the meet, then
+  //     each size's lexicographic (latency, gpu_id) argmin over its GPUs within
+  //     the warp (segments of W lanes, W = pow2ceil(n_gpus) clipped to 32); a warp
+  //     chunk's winner goes to part[(k - 1) * chunks + g / 32].
+  // check_violate's early exit and co-runner order do not change its boolean,
+  // and best_for is pure, so evaluating sizes the search never probes changes
+  // nothing.  The job covers sizes k0 + 1 .. k0 + kmax.
+  __device__ __forceinline__ void job_propose(int m, int k0, int kmax, int cprio, double dl, double front,
+                                              double now) const {
+    const int C1 = CONC + 1;
+    const int t = w * 32 + lane;
+    // A1. projections, items (k, g, c) from thread 0 up; the warps stay on one path
+    if (cf->use_violate) {
+      const int ni = kmax * NG * CONC;
+      for (int i = t; i < ni; i += NT) {
+        const int pg = i / CONC, c = i - pg * CONC;
+        const int kq = pg / NG, g = pg - kq * NG;
+        const int n = GI(GI_NRUN, g);
+        if (!(n < CONC)) continue;  // has_slot fails: phase B never reads this pair's items
+        bool v = false;
+        if (c < n) {
+          const int s = slot_at(g, c);
+          const int ep = SB(SB_PRIO, s);
+          if (ep <= cprio) {
+            Cand cd;
+#pragma unroll
+            for (int q = 0; q < NM; ++q) cd.c[q] = thr(m, k0 + kq + 1, q);
+            v = projection(s, cd, ep) > SD(SD_DL, s);
+          }
+        }
+        pv[pg * C1 + c] = v;
+      }
+    }
+    // A2. the pairs' LP-cap test + check_meet, items (k, g) from the last thread
+    // down, so that they fall on threads with no (or the fewest) projections
+    const int np2 = kmax * NG;
+    for (int pg = NT - 1 - t; pg < np2; pg += NT) {
+      const int kq = pg / NG, g = pg - kq * NG;
+      if (!(GI(GI_NRUN, g) < CONC)) continue;
+      Cand cd;
+      load_cand(m, k0 + kq + 1, cd);
+      bool capv = false;
+      if (cprio == 1) {
+        const double capf = GD(GD_CAPF, g);
+#pragma unroll
+        for (int q = 0; q < NM; ++q) capv |= GD(GD_LPA + q, g) + cd.c[q] > capf;
+      }
+      double assumed[NM];
+#pragma unroll
+      for (int q = 0; q < NM; ++q) assumed[q] = 0.5 * GD(GD_AGG + q, g);
+      const double intf = pr.predict(assumed, cd.cmp, cd.mem, cprio);
+      const double lat = cd.total + py_max(0.0, GD(GD_TAV, g) - now) + (intf - 1.0) * cd.kern + (now - front);
+      pm[pg] = (uint8_t)((lat <= dl ? 1 : 0) | (capv ? 2 : 0));
+      plat[pg] = lat;
+      pintf[pg] = intf;
+    }
+    RP_T(t_b);
+    cta_bar(3);
+    if (w == 0) RP_ADD(RPF_CTA_B, t_b);  // the master's wait at the end of phase A
+    const int lw = NG <= 1 ? 0 : 32 - __clz(NG - 1);
+    const int W = 1 << lw, seg = W < 32 ? W : 32, nch = Layout::cta_chunks(NG);
+    const int np = kmax << lw;
+    for (int b0 = w * 32; b0 < np; b0 += NT) {  // warp-uniform trip count
+      const int p = b0 + lane, kq = p >> lw, g = p & (W - 1);
+      bool found = false;
+      int bg = g;
+      double bl = 0.0, bi = 0.0;
+      if (kq < kmax && g < NG && GI(GI_NRUN, g) < CONC) {
+        const int pg = kq * NG + g;
+        const int f = pm[pg];
+        bool viol = false;
+        if (cf->use_violate) {
+          viol = (f & 2) != 0;
+          for (int c = 0; c < CONC; ++c) viol |= pv[pg * C1 + c] != 0;
+        }
+        found = !viol && !(cf->use_meet && !(f & 1));
+        bl = plat[pg];
+        bi = pintf[pg];
+      }
+      for (int off = seg >> 1; off; off >>= 1) {
+        const bool f2 = __shfl_xor_sync(kFull, found, off);
+        const int g2 = __shfl_xor_sync(kFull, bg, off);
+        const double l2 = __shfl_xor_sync(kFull, bl, off);
+        const double i2 = __shfl_xor_sync(kFull, bi, off);
+        if (f2 && (!found || l2 < bl || (l2 == bl && g2 < bg))) {
+          found = true;
+          bg = g2;
+          bl = l2;
+          bi = i2;
+        }
+      }
+      if ((lane & (seg - 1)) == 0 && kq < kmax) part[kq * nch + (g >> 5)] = Part{bl, bi, 0ull, found ? bg : -1, 0};
+    }
+    cta_bar(2);
+  }
+  // master side of JOB_PROPOSE: post it for sizes k0 + 1 .. k0 + kcnt and take part in it
+  __device__ __forceinline__ void run_propose_job(int m, int k0, int kcnt, int cprio, double dl, double front,
+                                                  double now) {
+    if (lane == 0) *jb = Job{JOB_PROPOSE, m, kcnt, cprio, k0, 0, now, dl, front};
+    RP_T(t_a);
+    post_job();
+    job_propose(m, k0, kcnt, cprio, dl, front, now);
+    RP_ADD(RPF_CTA_A, t_a);  // post + phases A and B (barrier-bound: the slowest warp)
+    RP_CNT(RPF_N_CTA);
+  }
+  // best of size index kq over its warp chunks, in GPU order (best_for's tie-break)
+  __device__ __forceinline__ bool size_best(int kq, int nch, int& bg, double& bl, double& bi) const {
+    bool found = false;
+    for (int ch = 0; ch < nch; ++ch) {
+      const Part q = part[kq * nch + ch];
+      if (q.g >= 0 && (!found || q.t < bl || (q.t == bl && q.g < bg))) {
+        found = true;
+        bg = q.g;
+        bl = q.t;
+        bi = q.x;
+      }
+    }
+    return found;
+  }
+  // PredictivePolicy.propose on the CTA.  When the (size x GPU x co-runner)
+  // items of every size fit in two passes of the CTA, one job evaluates all
+  // sizes and the binary search's probes are replayed on the feasibility bits
+  // (lane k - 1 holds size k).  Otherwise (C5's 64 GPUs) each probe is one job
+  // over its GPUs x co-runners, ~1 item per thread, in the search's order.
+  __device__ __forceinline__ int propose_cta(int m, int kmax, double now, Plan& plan) {
+    const double front = front_arrival(m);
+    const int cprio = mprio(m);
+    const double dl = mdeadline(m);
+    const int nch = Layout::cta_chunks(NG);
+    int lo = 1, hi = kmax, bestk = 0;
+    if (kmax * NG * (CONC + 1) > 2 * NT) {
+      while (lo <= hi) {
+        const int mid = (lo + hi) / 2;
+        run_propose_job(m, mid - 1, 1, cprio, dl, front, now);
+        int bg = 0;
+        double bl = 0.0, bi = 0.0;
+        if (size_best(0, nch, bg, bl, bi)) {
+          bestk = mid;
+          plan = Plan{true, bg, bl, bi};
+          lo = mid + 1;
+        } else {
+          hi = mid - 1;
+        }
+      }
+      return bestk;
+    }
+    run_propose_job(m, 0, kmax, cprio, dl, front, now);
+    RP_T(t_m);
+    bool found = false;
+    int bg = 0;
+    double bl = 0.0, bi = 0.0;
+    if (lane < kmax) found = size_best(lane, nch, bg, bl, bi);
+    const unsigned feas = __ballot_sync(kFull, found);  // bit k - 1: best_for(k) is not None
+    while (lo <= hi) {
+      const int mid = (lo + hi) / 2;
+      if (feas >> (mid - 1) & 1u) {
+        bestk = mid;
+        lo = mid + 1;
+      } else {
+        hi = mid - 1;
+      }
+    }
+    if (bestk) {
+      const int src = bestk - 1;
+      plan = Plan{true, __shfl_sync(kFull, bg, src), __shfl_sync(kFull, bl, src), __shfl_sync(kFull, bi, src)};
+    }
+    RP_ADD(RPF_CTA_M, t_m);
+    return bestk;
+  }
+
   // PredictivePolicy.propose (scheduler.py:257-285) + largest_feasible (:78-90).
   // When every size fits in the warp (kmax segments of W = pow2ceil(n_gpus)
   // lanes), all sizes are evaluated at once (lane = (k - 1) * W + g; best_for
@@ -794,6 +1068,8 @@ struct Sim : Geom<GEOM> {
   __device__ __forceinline__ int propose(int m, double now, Plan& plan) {
     const double front = front_arrival(m);
     const int kmax = min(q_len(m), mmaxb(m));
+    if constexpr (CTA)
+      if (kmax <= 32) return propose_cta(m, kmax, now, plan);
     const int cprio = mprio(m);
     const double dl = mdeadline(m);
     int lo = 1, hi = kmax, bestk = 0;
@@ -1002,41 +1278,102 @@ struct Sim : Geom<GEOM> {
     sync();
   }
 
+  // _ensure_timeout for every queue in model order (simulation.py:360-361)
+  __device__ __forceinline__ void ensure_timeouts(double now) {
+    RP_T(t_to);
+    for (int m0 = 0; m0 < M; m0 += 32) {
+      const int m = m0 + lane;
+      const bool need = m < M && q_len(m) > 0 && QI(QI_TGEN, m) != QI(QI_FGEN, m);
+      const unsigned mask = __ballot_sync(kFull, need);
+      if (need) {
+        const unsigned long long q = seq + 1 + __popc(mask & ((1u << lane) - 1));
+        ed[S + m] = py_max(now, front_arrival(m) + mtimeout(m));
+        ek[S + m] = ((unsigned long long)kTO << 56) | q;
+        QI(QI_EGEN, m) = QI(QI_FGEN, m);
+        QI(QI_TGEN, m) = QI(QI_FGEN, m);
+      }
+      seq += __popc(mask);
+    }
+    sync();
+    RP_ADD(RPF_TIMEOUTS, t_to);
+  }
+
   // Simulation._pass (simulation.py:301-361) + run_scheduling_pass (scheduler.py:355-378)
   __device__ __forceinline__ void do_pass(double now) {
     const int pass_id = ++pass_seq;
     ++c_passes;
-    const bool predictive = policy() == STRAIT_POLICY_PREDICTIVE;
     if (policy() == STRAIT_POLICY_REACTIVE) reactive_catch_up(now);  // begin_pass (baselines.py:113-114)
-    // queue_order (scheduler.py:249-255): stable sort of the ready queues by
-    // (priority, front arrival, model_id), as a lane-parallel rank sort.
-    // key = priority in the top bit | bit pattern of the (>= 0) front arrival;
-    // queues that are not ready get ~0 and sort last.
+    // The queues this pass acts on: a front that early_drop removes, or an
+    // eligible queue (TaskQueue.eligible).  A queue's front and length change
+    // only when the pass reaches that queue (its own drop / submission), so both
+    // tests give at the pass start what they give when the loop reaches it; a
+    // ready queue in neither set is a no-op of the loop and is skipped.
     RP_T(t_rank);
-    unsigned long long* qk = reinterpret_cast<unsigned long long*>(qd);
-    const bool use_prio = cf->use_priority_order;
-    for (int m = lane; m < M; m += 32) {
-      const bool rdy = q_len(m) > 0;
-      qk[m] = rdy ? ((unsigned long long)(use_prio ? mprio(m) : 0) << 63) |
-                        (unsigned long long)__double_as_longlong(front_arrival(m))
-                  : kNoKey;
-    }
-    sync();
-    int n = 0;
+    unsigned long long act = 0, dropm = 0;
     for (int m0 = 0; m0 < M; m0 += 32) {
       const int m = m0 + lane;
-      const unsigned long long km = m < M ? qk[m] : kNoKey;
-      const bool rdy = km != kNoKey;
-      if (rdy) {
-        int rank = 0;
-#pragma unroll 1
-        for (int j = 0; j < M; ++j) {
-          const unsigned long long kj = qk[j];
-          rank += kj < km || (kj == km && j < m);
+      bool d = false, e = false;
+      if (m < M) {
+        const int len = q_len(m);
+        if (len) {
+          const double fr = front_arrival(m);
+          d = (fr + mdeadline(m)) - now < tab_total(m, 1);  // early_drop's front test (scheduler.py:65-75)
+          e = len >= mmaxb(m) || now >= fr + mtimeout(m);
         }
-        QI(QI_ORD, rank) = m;
       }
-      n += __popc(__ballot_sync(kFull, rdy));
+      dropm |= (unsigned long long)__ballot_sync(kFull, d) << m0;
+      act |= (unsigned long long)__ballot_sync(kFull, d || e) << m0;
+    }
+    RP_ADD(RPF_RANK, t_rank);
+    if (act) pass_queues(now, act, dropm, pass_id);
+    ensure_timeouts(now);
+  }
+
+  // the acted-on queues of a pass, in queue order: early drop, then at most one
+  // submission per eligible queue (run_scheduling_pass, scheduler.py:355-378)
+  __device__ __forceinline__ void pass_queues(double now, unsigned long long act, unsigned long long dropm,
+                                              int pass_id) {
+    RP_T(t_rank);
+    const bool predictive = policy() == STRAIT_POLICY_PREDICTIVE;
+    // queue_order (scheduler.py:249-255): stable sort of the acted-on ready
+    // queues by (priority, front arrival, model_id) — the order their subset
+    // has in the sort of all ready queues — as a lane-parallel rank sort.
+    // key = priority in the top bit | bit pattern of the (>= 0) front arrival.
+    const bool use_prio = cf->use_priority_order;
+    const int n = __popcll(act);
+    if (M <= 32) {  // keys in registers, broadcast by shuffles
+      const bool on = lane < M && (act >> lane & 1);
+      const unsigned long long km =
+          on ? ((unsigned long long)(use_prio ? mprio(lane) : 0) << 63) |
+                   (unsigned long long)__double_as_longlong(front_arrival(lane))
+             : kNoKey;
+      int rank = 0;
+#pragma unroll 4
+      for (int j = 0; j < M; ++j) {
+        const unsigned long long kj = __shfl_sync(kFull, km, j);
+        rank += kj < km || (kj == km && j < lane);
+      }
+      __syncwarp();
+      if (on) QI(QI_ORD, rank) = lane;
+    } else {
+      unsigned long long* qk = reinterpret_cast<unsigned long long*>(qd);
+      for (int m = lane; m < M; m += 32)
+        qk[m] = act >> m & 1 ? ((unsigned long long)(use_prio ? mprio(m) : 0) << 63) |
+                                   (unsigned long long)__double_as_longlong(front_arrival(m))
+                             : kNoKey;
+      sync();
+      for (int m = lane; m < M; m += 32) {
+        const unsigned long long km = qk[m];
+        if (km != kNoKey) {
+          int rank = 0;
+#pragma unroll 1
+          for (int j = 0; j < M; ++j) {
+            const unsigned long long kj = qk[j];
+            rank += kj < km || (kj == km && j < m);
+          }
+          QI(QI_ORD, rank) = m;
+        }
+      }
     }
     sync();
     RP_ADD(RPF_RANK, t_rank);
@@ -1049,12 +1386,13 @@ struct Sim : Geom<GEOM> {
       const int m = QI(QI_ORD, i);
       RP_T(t_drop);
       RP_CNT(RPF_N_QUEUES);
-      early_drop(m, now);
+      if (dropm >> m & 1) early_drop(m, now);
       RP_ADD(RPF_DROP, t_drop);
       RP_T(t_elig);
       const int len = q_len(m);
       if (!len) continue;
-      if (!(len >= mmaxb(m) || now >= front_arrival(m) + mtimeout(m))) continue;  // TaskQueue.eligible
+      // TaskQueue.eligible: known from the pass start unless the drop moved the front
+      if ((dropm >> m & 1) && !(len >= mmaxb(m) || now >= front_arrival(m) + mtimeout(m))) continue;
       RP_CNT(RPF_N_ELIGIBLE);
       if (!any_slot) continue;
       if (predictive && !icur_ready) {
@@ -1077,23 +1415,6 @@ struct Sim : Geom<GEOM> {
       RP_ADD(RPF_ICUR, t_icur);
       any_slot = has_any_slot();
     }
-    RP_T(t_to);
-    // _ensure_timeout for every queue in model order (simulation.py:360-361)
-    for (int m0 = 0; m0 < M; m0 += 32) {
-      const int m = m0 + lane;
-      const bool need = m < M && q_len(m) > 0 && QI(QI_TGEN, m) != QI(QI_FGEN, m);
-      const unsigned mask = __ballot_sync(kFull, need);
-      if (need) {
-        const unsigned long long q = seq + 1 + __popc(mask & ((1u << lane) - 1));
-        ed[S + m] = py_max(now, front_arrival(m) + mtimeout(m));
-        ek[S + m] = ((unsigned long long)kTO << 56) | q;
-        QI(QI_EGEN, m) = QI(QI_FGEN, m);
-        QI(QI_TGEN, m) = QI(QI_FGEN, m);
-      }
-      seq += __popc(mask);
-    }
-    sync();
-    RP_ADD(RPF_TIMEOUTS, t_to);
   }
 
   // ------------------------------------------------------------ event handlers
@@ -1232,6 +1553,7 @@ struct Sim : Geom<GEOM> {
         if (whole > 0) {
           cap = py_min(cf->aimd_ceiling, old + whole * cf->aimd_increase);
           GD(GD_CAP, g) = cap;
+          GD(GD_CAPF, g) = MathT::div(cap, 100.0);
           GD(GD_TICK, g) = last + whole * cf->aimd_interval;
         }
         changed = cap != old;
@@ -1242,6 +1564,62 @@ struct Sim : Geom<GEOM> {
     }
     sync();
     fail_any(bad, STRAIT_EINVAL);
+  }
+
+  // ------------------------------------------------------------ next event
+  // this thread's share of the event homes: i = first, first + step, ...
+  __device__ __forceinline__ void scan_homes(int first, int step, double& bt, unsigned long long& bk, int& bi) const {
+#pragma unroll 1
+    for (int i = first; i < NE; i += step) {
+      const double t = ed[i];
+      const unsigned long long kk = ek[i];
+      if (t < bt || (t == bt && kk < bk)) bt = t, bk = kk, bi = i;
+    }
+  }
+  // across lanes: event times are >= 0, so their bit patterns order like the
+  // values; a 128-bit (time, key) minimum as four 32-bit warp reductions.
+  // Leaves the minimum and its home in every lane.
+  __device__ __forceinline__ void warp_min_event(double& bt, unsigned long long& bk, int& bi) const {
+    const unsigned long long tb = (unsigned long long)__double_as_longlong(bt);
+    const unsigned w0 = (unsigned)(tb >> 32), w1 = (unsigned)tb, w2 = (unsigned)(bk >> 32), w3 = (unsigned)bk;
+    const unsigned m0 = __reduce_min_sync(kFull, w0);
+    bool c = w0 == m0;
+    const unsigned m1 = __reduce_min_sync(kFull, c ? w1 : ~0u);
+    c = c && w1 == m1;
+    const unsigned m2 = __reduce_min_sync(kFull, c ? w2 : ~0u);
+    c = c && w2 == m2;
+    const unsigned m3 = __reduce_min_sync(kFull, c ? w3 : ~0u);
+    c = c && w3 == m3;
+    bk = ((unsigned long long)m2 << 32) | m3;
+    bt = __longlong_as_double((long long)(((unsigned long long)m0 << 32) | m1));
+    bi = __shfl_sync(kFull, bi, __ffs(__ballot_sync(kFull, c)) - 1);
+  }
+  // JOB_SELECT (every warp of the CTA): warp w's minimum into part[w]
+  __device__ __forceinline__ void job_select() const {
+    double bt = __longlong_as_double(0x7ff0000000000000LL);
+    unsigned long long bk = kNoKey;
+    int bi = -1;
+    scan_homes(w * 32 + lane, NT, bt, bk, bi);
+    warp_min_event(bt, bk, bi);
+    if (lane == 0) part[w] = Part{bt, 0.0, bk, bi, 0};
+    cta_bar(2);
+  }
+
+  // helper warps (NW > 1): parked on barrier 1 until the master posts a job
+  __device__ void helper_loop() {
+    for (;;) {
+      cta_bar(1);
+      const int kind = jb->kind;
+      if (kind == JOB_EXIT) return;
+      const double now = jb->now;
+      if (kind == JOB_SELECT) {
+        job_select();
+        continue;
+      }
+      load_shared_pred();
+      if (kind == JOB_ICUR) job_icur(now);
+      else job_propose(jb->m, jb->k0, jb->kmax, jb->cprio, jb->dl, jb->front, now);
+    }
   }
 
   // ------------------------------------------------------------ main loop (simulation.py:475-513)
@@ -1256,6 +1634,7 @@ struct Sim : Geom<GEOM> {
     for (int g = lane; g < G; g += 32) {
       GD(GD_TAV, g) = 0.0;
       GD(GD_CAP, g) = cf->aimd_floor;
+      GD(GD_CAPF, g) = MathT::div(cf->aimd_floor, 100.0);
       GD(GD_TICK, g) = 0.0;
       GI(GI_NRUN, g) = 0;
       GI(GI_PHEAD, g) = 0;
@@ -1291,7 +1670,7 @@ struct Sim : Geom<GEOM> {
     for (int64_t i = lane; i < N; i += 32) A->req_status[base + i] = 0;
     for (int g = lane; g < NG; g += 32) cap_row_at(g, 0.0, g, cf->aimd_floor);  // simulation.py:196-197
     sync();
-    pr.load(P, cf->effect_cap);
+    load_pred();
     c_cap_rows = NG;
     seq = (unsigned long long)N;  // the arrivals took seq 1..N (simulation.py:184-194)
     next_arr = 0;
@@ -1313,30 +1692,23 @@ struct Sim : Geom<GEOM> {
       double bt = INF;
       unsigned long long bk = kNoKey;
       int bi = -1;
-#pragma unroll 1
-      for (int i = lane; i < NE; i += 32) {
-        const double t = ed[i];
-        const unsigned long long kk = ek[i];
-        if (t < bt || (t == bt && kk < bk)) bt = t, bk = kk, bi = i;
+      bool wide = false;
+      if constexpr (CTA) wide = NE > 32;
+      if (wide) {  // JOB_SELECT: every warp scans a share of the homes; lane w takes warp w's minimum
+        if (lane == 0) jb->kind = JOB_SELECT;
+        post_job();
+        job_select();
+        if (lane < NW) {
+          const Part q = part[lane];
+          bt = q.t;
+          bk = q.key;
+          bi = q.g;
+        }
+      } else {
+        scan_homes(lane, 32, bt, bk, bi);
       }
-      // across lanes: event times are >= 0, so their bit patterns order like the
-      // values; a 128-bit (time, key) minimum as four 32-bit warp reductions
-      {
-        const unsigned long long tb = (unsigned long long)__double_as_longlong(bt);
-        const unsigned w0 = (unsigned)(tb >> 32), w1 = (unsigned)tb, w2 = (unsigned)(bk >> 32), w3 = (unsigned)bk;
-        const unsigned m0 = __reduce_min_sync(kFull, w0);
-        bool c = w0 == m0;
-        const unsigned m1 = __reduce_min_sync(kFull, c ? w1 : ~0u);
-        c = c && w1 == m1;
-        const unsigned m2 = __reduce_min_sync(kFull, c ? w2 : ~0u);
-        c = c && w2 == m2;
-        const unsigned m3 = __reduce_min_sync(kFull, c ? w3 : ~0u);
-        c = c && w3 == m3;
-        bk = ((unsigned long long)m2 << 32) | m3;
-        if (bk == kNoKey) break;
-        bt = __longlong_as_double((long long)(((unsigned long long)m0 << 32) | m1));
-        bi = __shfl_sync(kFull, bi, __ffs(__ballot_sync(kFull, c)) - 1);
-      }
+      warp_min_event(bt, bk, bi);
+      if (bk == kNoKey) break;
       sync();  // the scan's reads of the event homes complete before any handler writes them
       RP_ADD(RPF_SELECT, t_sel);
       RP_T(t_h);
@@ -1397,6 +1769,10 @@ struct Sim : Geom<GEOM> {
       }
       RP_ADD(RPF_POST, t_post);
     }
+    if constexpr (CTA) {  // release the helper warps (the loop's only exit is above)
+      if (lane == 0) jb->kind = JOB_EXIT;
+      post_job();
+    }
 #if STRAIT_REPLAY_PROFILE
     RP_ADD(RPF_TOTAL, t_all);
     if (lane == 0)
@@ -1435,27 +1811,31 @@ struct Sim : Geom<GEOM> {
 // MINB = minimum resident CTAs of 4 warps per SM: 1 lets ptxas keep the whole
 // replay state in registers (latency: few replays), 4 caps it at 128 registers
 // for 16 resident replays per SM (throughput: replay sweeps).
-template <int NM, int MINB, bool TR, bool LEAN, int GEOM>
-__global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant__ StraitReplayArgs a, int wpc) {
+// NW = 1: up to wpc replays per CTA, one warp each.  NW > 1: one replay per
+// CTA of NW warps (warp 0 the master, the others helpers).
+template <int NM, int MINB, bool TR, bool LEAN, int GEOM, int NW>
+__global__ void __launch_bounds__(NW > 1 ? 32 * NW : 128, MINB)
+    replay_kernel(const __grid_constant__ StraitReplayArgs a, int wpc) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int w = threadIdx.x >> 5;
-  const int64_t slot_w = (int64_t)blockIdx.x * wpc + w;
+  const int64_t slot_w = NW > 1 ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * wpc + w;
   if (slot_w >= a.n_replays) return;
   const int64_t r = a.order ? (int64_t)a.order[slot_w] : slot_w;
-  const Layout L(a.max_gpus, a.max_concurrency, a.models.n_models, NM);
-  unsigned char* base = smem + (size_t)w * L.bytes;
-  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type, TR, LEAN, GEOM> S;
+  const Layout L(a.max_gpus, a.max_concurrency, a.models.n_models, NM, NW, a.models.stride);
+  unsigned char* base = NW > 1 ? smem : smem + (size_t)w * L.bytes;
+  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type, TR, LEAN, GEOM, NW> S;
   S.A = &a;
   S.cf = a.cfg + r;
   S.lane = threadIdx.x & 31;
+  S.w = NW > 1 ? w : 0;
   S.r = r;
   if (!S.set_geom(L, S.cf, a.models.stride)) {  // the launcher chose a fixed geometry this replay does not have
-    if (S.lane == 0) {
+    if (S.lane == 0 && S.w == 0) {
       int64_t* c = a.counters + r * STRAIT_RC_N;
       for (int i = 0; i < STRAIT_RC_N; ++i) c[i] = 0;
       c[STRAIT_RC_ERROR] = STRAIT_EINVAL;
     }
-    return;
+    return;  // uniform over the CTA when NW > 1: no helper is left parked
   }
   S.base = a.req_off[r];
   S.N = a.req_off[r + 1] - S.base;
@@ -1473,6 +1853,16 @@ __global__ void __launch_bounds__(128, MINB) replay_kernel(const __grid_constant
   S.sb = (int8_t*)(base + L.sb);
   S.go = (int8_t*)(base + L.go);
   S.qb = (int8_t*)(base + L.qb);
+  S.jb = (Job*)(base + L.jb);
+  S.pv = (uint8_t*)(base + L.pv);
+  S.pm = (uint8_t*)(base + L.pm);
+  S.plat = (double*)(base + L.plat);
+  S.pintf = (double*)(base + L.pintf);
+  S.part = (Part*)(base + L.part);
+  if (NW > 1 && w > 0) {
+    S.helper_loop();
+    return;
+  }
   S.batch_seq = S.pass_seq = S.done_order = S.err = 0;
   S.lp_allowance = S.cf->reactive_default;
   S.last_reset = 0.0;
@@ -1502,18 +1892,28 @@ inline bool c5_geometry(const StraitReplayArgs& a) {
 
 // host side: launch one instantiation (explicitly specialised in strait_replay_nm*.cu);
 // minb = 4 selects the 128-register throughput variant, 0 the traced latency variant,
-// else the latency variant
+// 2 the CTA-per-replay latency variant (kCtaWarps warps per replay), else the
+// one-warp latency variant
+constexpr int kCtaWarps = 8;
+
 template <int NM>
 int launch_replay(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb);
 
-template <int NM, int MINB, bool TR, bool LEAN, int GEOM>
+// shared memory of one CTA-per-replay replay (0: more than the opt-in maximum)
+inline size_t cta_replay_smem(const StraitReplayArgs& a) {
+  const size_t b = Layout(a.max_gpus, a.max_concurrency, a.models.n_models, a.models.n_metrics, kCtaWarps,
+                          a.models.stride).bytes;
+  return b <= 227 * 1024 ? b : 0;
+}
+
+template <int NM, int MINB, bool TR, bool LEAN, int GEOM, int NW = 1>
 int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) {
-  const size_t smem = smem_per_warp * wpc;
-  if (cudaFuncSetAttribute(replay_kernel<NM, MINB, TR, LEAN, GEOM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
+  const size_t smem = NW > 1 ? cta_replay_smem(a) : smem_per_warp * wpc;
+  auto* k = replay_kernel<NM, MINB, TR, LEAN, GEOM, NW>;
+  if (!smem || cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return set_error(STRAIT_ECUDA, "strait_replay: cannot reserve %zu B of shared memory", smem);
-  const unsigned grid = (unsigned)((a.n_replays + wpc - 1) / wpc);
-  replay_kernel<NM, MINB, TR, LEAN, GEOM><<<grid, 32 * wpc, smem, st>>>(a, wpc);
+  const unsigned grid = NW > 1 ? (unsigned)a.n_replays : (unsigned)((a.n_replays + wpc - 1) / wpc);
+  k<<<grid, NW > 1 ? 32 * NW : 32 * wpc, smem, st>>>(a, wpc);
   return check_launch("strait_replay");
 }
 
@@ -1521,6 +1921,15 @@ int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_
   template <>                                                                                                     \
   int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb) { \
     const bool po = lean_batch(a);                                                                                \
+    if (minb == 2) { /* CTA per replay: single replays and few-replay launches */                                \
+      if constexpr (NMV == 5) {                                                                                   \
+        if (c5_geometry(a)) return launch_replay_occ<NMV, 1, false, false, 3, kCtaWarps>(a, st, wpc, smem_per_warp); \
+        if (po && overload_geometry(a) && a.models.stride == 8)                                                   \
+          return launch_replay_occ<NMV, 1, false, true, 2, kCtaWarps>(a, st, wpc, smem_per_warp);                \
+      }                                                                                                           \
+      return po ? launch_replay_occ<NMV, 1, false, true, 0, kCtaWarps>(a, st, wpc, smem_per_warp)                \
+                : launch_replay_occ<NMV, 1, false, false, 0, kCtaWarps>(a, st, wpc, smem_per_warp);              \
+    }                                                                                                             \
     if constexpr (NMV == 5) /* traced: run() / Simulation.run() of the overload geometry */                     \
       if (minb == 0 && po && overload_geometry(a) && a.models.stride == 8)                                       \
         return launch_replay_occ<NMV, 1, true, true, 2>(a, st, wpc, smem_per_warp);                             \

@@ -1,0 +1,4 @@
+nvidia-smi -L
+timeout 900 python scripts/cta_probe.py 2000 20000 > gpurun_out/cta_probe.txt 2>&1; echo probe rc=$?; cat gpurun_out/cta_probe.txt | cut -c1-400
+timeout 900 python -m pytest tests/test_replay_cta_gpu.py -q -x -p no:cacheprovider > gpurun_out/pytest_cta.txt 2>&1; tail -3 gpurun_out/pytest_cta.txt
+STRAIT_LIB=build/prof/_strait.so timeout 600 python scripts/replay_profile.py 3000 2.5 20000 > gpurun_out/replay_profile.txt 2>&1; cat gpurun_out/replay_profile.txt

@@ -32,7 +32,7 @@ def main():
     lib.strait_replay_profile.restype = C.c_int
     for name, cfg in cases:
         b = ReplayBatch([ReplaySpec(cfg)])
-        out = np.zeros(24, np.uint64)
+        out = np.zeros(28, np.uint64)
         lib.strait_replay_profile(out.ctypes.data)  # reset
         res = b.run(metrics=False)
         lib.strait_replay_profile(out.ctypes.data)
@@ -48,6 +48,10 @@ def main():
         p = c[RC['PASSES']]
         print(f"  per pass: queues visited {out[16] / p:.2f}, eligible {out[17] / p:.2f}, wide proposes "
               f"{out[18] / p:.2f}, submits {out[19] / p:.2f}, icur_all {out[20] / p:.2f}")
+        nc = max(int(out[27]), 1)
+        if out[27]:
+            print(f"  CTA proposes {out[27]}: post..join {out[24] / nc:.0f} cyc (master wait at phase A end "
+                  f"{out[25] / nc:.0f}), master combine {out[26] / nc:.0f} cyc")
         w = max(int(out[18]), 1)
         print(f"  per wide propose: mean kmax {out[21] / w:.2f}, no GPU with a slot {100 * out[22] / w:.1f}%, "
               f"running entries {out[23] / w:.2f}")
