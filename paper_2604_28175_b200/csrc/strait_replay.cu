@@ -65,10 +65,13 @@ extern "C" int strait_replay(const StraitReplayArgs* a, void* stream) {
     return set_error(STRAIT_EINVAL, "strait_replay: concurrency_limit %d outside 1..%d", a->max_concurrency,
                      kMaxConc);
   if (a->max_gpus < 1) return set_error(STRAIT_EINVAL, "strait_replay: max_gpus < 1");
-  const int64_t per_warp = strait_replay_smem_bytes(a->max_gpus, a->max_concurrency, md.n_models, md.n_metrics);
-  if (!per_warp)
+  int64_t per_warp = strait_replay_smem_bytes(a->max_gpus, a->max_concurrency, md.n_models, md.n_metrics);
+  // a geometry past the one-warp budget still runs as one replay per CTA (up to the 227 KB opt-in maximum)
+  const bool cta_only = !per_warp && a->n_replays <= (int64_t)sm_count() && cta_replay_smem(*a);
+  if (!per_warp && !cta_only)
     return set_error(STRAIT_EINVAL, "strait_replay: %d GPUs x %d slots x %d models needs more than %zu B on chip",
                      a->max_gpus, a->max_concurrency, md.n_models, kSmemBudget);
+  if (cta_only) per_warp = (int64_t)cta_replay_smem(*a);
   const void* need[] = {a->cfg, a->req_off, a->arr_time, a->arr_model, a->model_req, a->mr_off, a->noise,
                         a->bc1, a->bc2, a->pred_state, a->pred_step, a->req_status, a->req_violated,
                         a->req_completion, a->req_batch, a->dec_time, a->dec_pass, a->dec_model, a->dec_size,
@@ -92,7 +95,8 @@ extern "C" int strait_replay(const StraitReplayArgs* a, void* stream) {
   // replays over SMs and sub-partitions; past that, the 16-replays-per-SM kernel
   // a traced launch (event log) always runs the latency variant with the log compiled in
   int minb = a->trace ? 0 : replay_occupancy(a->n_replays, wpc);
-  if (minb < 4) wpc = 1;
+  if (minb < 4 || cta_only) wpc = 1;
+  if (cta_only) minb = a->trace ? 3 : 2;
   // at most one replay per SM and more running-batch slots than a warp has lanes (C5's 64 GPUs):
   // a CTA of kCtaWarps warps per replay (STRAIT_REPLAY_NW=8 forces it, =1 disables it)
   if (minb == 1 && a->n_replays <= (int64_t)sm_count() && cta_replay_smem(*a) &&

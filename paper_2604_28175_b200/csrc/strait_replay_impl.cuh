@@ -97,7 +97,7 @@ struct FullInlineMath : InlineMath {
 constexpr int kKC = 0, kTC = 1, kARR = 2, kTO = 3, kTICK = 4;  // simulation.py:28-33 tie ranks
 constexpr double kWorkEps = 1e-9;                               // simulation.py:35
 constexpr unsigned long long kNoKey = ~0ULL;
-constexpr int kMaxConc = 8;
+constexpr int kMaxConc = 32;  // lane-per-list-position steps (recompute, restamp, intf_cur of a GPU)
 constexpr int kMaxModels = 64;
 constexpr int kMaxBatch = 64;
 constexpr unsigned kFull = 0xffffffffu;
@@ -283,6 +283,9 @@ struct Sim : Geom<GEOM> {
   int lp_allowance;   // ReactiveState (baselines.py:81-110)
   double last_reset;
   int64_t next_arr, resolved;
+  int64_t pf_q, pf_g;  // the last arrival's queue-order check, settled at the next arrival / the end
+  int pf_m;            // model of the next arrival
+  double pf_t2;        // time of the arrival after the next
   int64_t c_batches, c_completed, c_passes, c_cap_rows, c_events, c_hp_viol, c_lp_viol, c_hp_drop, c_lp_drop;
   int64_t c_trace;  // trace records produced (TR)
 #if STRAIT_REPLAY_PROFILE
@@ -1468,6 +1471,9 @@ struct Sim : Geom<GEOM> {
     const int g = SI(SI_GPU, s), j = SI(SI_J, s);
     const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s), prio = SB(SB_PRIO, s);
     const int bid = SI(SI_BID, s), req0 = SI(SI_REQ0, s);
+    // the batch's (first 32) requests: global index and arrival time are loaded
+    // here and consumed after the bookkeeping below, which hides their latency
+    const int64_t g_pre = lane < k ? req_at(req0 + lane) : 0;
     bool ok = true;
     const double seg_d = now - SD(SD_LAST, s), seg_slow = SD(SD_SLOW, s);
     sync();
@@ -1475,16 +1481,22 @@ struct Sim : Geom<GEOM> {
     if (seg_d > 0) trace1(STRAIT_TR_SEGMENT, now, g, bid, -1, 0, seg_d, seg_slow);  // ExecutionState.finish
     fail_any(!ok, STRAIT_EORDER);
     sync();
+    const double a_pre = lane < k ? arr(g_pre) : 0.0;
     const double measured = now - SD(SD_KS, s);
     const double completion = now + (tab_total(m, k) - tab_transfer(m, k) - tab_kernel(m, k));
     const double dl = mdeadline(m);
+    double tw[NM];
+    tl_twa(s, now, tw);
+    const double tk = tab_kernel(m, k);
+    const double actual = MathT::div(measured, tk);
+    if (!(actual > 0)) fail(STRAIT_EINVAL);
     int nviol = 0;
     for (int i0 = 0; i0 < k; i0 += 32) {
       const int i = i0 + lane;
       bool viol = false;
       if (i < k) {
-        const int64_t gidx = req_at(req0 + i);
-        viol = completion > arr(gidx) + dl;
+        const int64_t gidx = i0 ? req_at(req0 + i) : g_pre;
+        viol = completion > (i0 ? arr(gidx) : a_pre) + dl;
         A->req_status[gidx] = 1;
         A->req_violated[gidx] = (uint8_t)viol;
         A->req_completion[gidx] = completion;
@@ -1495,11 +1507,6 @@ struct Sim : Geom<GEOM> {
     resolved += k;
     if (prio == 0) c_hp_viol += nviol;
     else c_lp_viol += nviol;
-    double tw[NM];
-    tl_twa(s, now, tw);
-    const double tk = tab_kernel(m, k);
-    const double actual = MathT::div(measured, tk);
-    if (!(actual > 0)) fail(STRAIT_EINVAL);
     // GpuRuntimeState.remove_entry (runtime.py:132-141): shift the running list
     const int n = GI(GI_NRUN, g);
     int pos = 0;
@@ -1674,6 +1681,9 @@ struct Sim : Geom<GEOM> {
     c_cap_rows = NG;
     seq = (unsigned long long)N;  // the arrivals took seq 1..N (simulation.py:184-194)
     next_arr = 0;
+    pf_q = pf_g = 0;
+    pf_m = N ? (int)__ldg(&A->arr_model[base]) : 0;
+    pf_t2 = N > 1 ? arr(base + 1) : INF;
     if (N) {
       push_event(S + M, cf->aimd_interval, kTICK);
       put(ed[S + M + 1], arr(base));
@@ -1721,13 +1731,20 @@ struct Sim : Geom<GEOM> {
       int post_timeout = -1;
       bool post_tick = false;
       if (kind == kARR) {  // _on_arrival (simulation.py:365-371)
+        // the arrival stream is read one arrival ahead (pf_m, pf_t2), and the
+        // queue-order check of the previous arrival is settled now, so no
+        // global load is waited on here
+        if (pf_q != pf_g) fail(STRAIT_EINVAL);  // per-model arrivals must pop in k order
         const int64_t gidx = base + next_arr;
+        const int m = pf_m;
         ++next_arr;
-        put(ed[S + M + 1], next_arr < N ? arr(base + next_arr) : INF);
+        put(ed[S + M + 1], next_arr < N ? pf_t2 : INF);
         put(ek[S + M + 1], next_arr < N ? (unsigned long long)kARR << 56 : kNoKey);
-        const int m = __ldg(&A->arr_model[gidx]);
+        pf_m = next_arr < N ? (int)__ldg(&A->arr_model[base + next_arr]) : 0;
+        pf_t2 = next_arr + 1 < N ? arr(base + next_arr + 1) : INF;
         const int t = QI(QI_TAIL, m);
-        if (req_at(t) != gidx) fail(STRAIT_EINVAL);  // per-model arrivals must pop in k order
+        pf_q = req_at(t);
+        pf_g = gidx;
         put(QI(QI_TAIL, m), t + 1);
         if (t + 1 - QI(QI_HEAD, m) == 1) {  // TaskQueue.push into an empty queue: new front
           put(QI(QI_FGEN, m), QI(QI_FGEN, m) + 1);
@@ -1778,6 +1795,7 @@ struct Sim : Geom<GEOM> {
     if (lane == 0)
       for (int i = 0; i < RPF_N; ++i) atomicAdd(&g_replay_prof[i], (unsigned long long)prof[i]);
 #endif
+    if (pf_q != pf_g) fail(STRAIT_EINVAL);  // the last arrival's queue-order check
     if (!err && resolved != N) err = STRAIT_EORDER;  // unresolved requests (simulation.py:491-494)
     sync();
     double* so = A->pred_state + r * 3 * np;
@@ -1892,8 +1910,9 @@ inline bool c5_geometry(const StraitReplayArgs& a) {
 
 // host side: launch one instantiation (explicitly specialised in strait_replay_nm*.cu);
 // minb = 4 selects the 128-register throughput variant, 0 the traced latency variant,
-// 2 the CTA-per-replay latency variant (kCtaWarps warps per replay), else the
-// one-warp latency variant
+// 2 the CTA-per-replay latency variant (kCtaWarps warps per replay), 3 its traced
+// form (geometries past the one-warp shared-memory budget), else the one-warp
+// latency variant
 constexpr int kCtaWarps = 8;
 
 template <int NM>
@@ -1921,6 +1940,8 @@ int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_
   template <>                                                                                                     \
   int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb) { \
     const bool po = lean_batch(a);                                                                                \
+    if (minb == 3) /* traced, geometry past the one-warp budget: CTA per replay with the event log */           \
+      return launch_replay_occ<NMV, 1, true, false, 0, kCtaWarps>(a, st, wpc, smem_per_warp);                    \
     if (minb == 2) { /* CTA per replay: single replays and few-replay launches */                                \
       if constexpr (NMV == 5) {                                                                                   \
         if (c5_geometry(a)) return launch_replay_occ<NMV, 1, false, false, 3, kCtaWarps>(a, st, wpc, smem_per_warp); \

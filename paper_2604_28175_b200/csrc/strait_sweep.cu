@@ -29,6 +29,7 @@ namespace strait {
 
 constexpr int kSweepThreads = 256;       // compute threads per CTA (one per triple)
 constexpr int kMaxStages = 4;
+constexpr int kMaxGroups = 3;  // consumer groups of 8 warps (named barriers 1 .. 15)
 
 // A *tile* is the unit one CTA processes at a time: `spb` consecutive segments
 // (all of their pairs and triples), contiguous in every SoA field array.
@@ -410,8 +411,10 @@ __device__ __forceinline__ int build_copy_table(const StraitSweepArgs& a, const 
 
 // SG != 0 fixes gpus_per_segment at compile time (SG * C == 256: one segment per
 // tile) so every shared-memory offset folds into an immediate.
-template <int NM, int C, int SG>
-__global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
+// MAXG = most consumer groups the instantiation runs: 2 (<= 113 registers, up to
+// 2 CTAs of one group per SM) or 3 (one CTA of 3 groups, <= 78 registers).
+template <int NM, int C, int SG, int MAXG = 2>
+__global__ void __launch_bounds__(32 * (8 * MAXG + 2), 1)
     sweep_ws_kernel(const StraitSweepArgs a, const StraitRefitArgs r, int with_refit, int nstages, int groups,
                     int diag, const __grid_constant__ CUtensorMap ent_map,
                     const __grid_constant__ CUtensorMap pair_map, int use_tmap) {
@@ -520,7 +523,7 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
   int64_t tile = blockIdx.x + (int64_t)group * gridDim.x;
   const int64_t tile_step = (int64_t)groups * gridDim.x;
   // st = k % nstages and use = k / nstages for k = group, group + groups, ...,
-  // kept incrementally (groups <= 2 <= nstages: at most one wrap per step)
+  // kept incrementally (groups <= nstages: at most one wrap per step)
   int st = group % nstages;
   uint32_t use = (uint32_t)(group / nstages);
   for (; tile < ntiles;
@@ -652,7 +655,7 @@ __global__ void __launch_bounds__(32 * (8 * 2 + 2), 1)
         s_intf[pp] = intf;
         s_adm[pp] = admitted;
       }
-      if (npw > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + 2 * kMaxStages + group), "r"(npw * 32) : "memory");
+      if (npw > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + kMaxGroups * kMaxStages + group), "r"(npw * 32) : "memory");
     }
 
     // ---- 3. warp 0: best_for argmin per segment ----
@@ -856,16 +859,18 @@ static int launch_sweep_c(const StraitSweepArgs& a, cudaStream_t st, const Strai
   const int force = env_int("STRAIT_SWEEP_PATH", 0);  // 0 auto, 1 sync, 3 bulk copies without tensor maps
   const bool use_tma = force == 1 ? false : tma_eligible(a, tg);
   if (use_tma) {
-    int ns = env_int("STRAIT_SWEEP_STAGES", 2);
-    ns = ns < 2 ? 2 : (ns > kWsMaxStages ? kWsMaxStages : ns);
     int groups = env_int("STRAIT_SWEEP_GROUPS", 1);
-    groups = groups < 1 ? 1 : (groups > 2 ? 2 : groups);
+    groups = groups < 1 ? 1 : (groups > kMaxGroups ? kMaxGroups : groups);
+    int ns = env_int("STRAIT_SWEEP_STAGES", groups > 2 ? 4 : 2);
+    ns = ns < 2 ? 2 : (ns > kWsMaxStages ? kWsMaxStages : ns);
+    if (ns < groups) ns = groups;  // every group owns a stage in flight
     const WsLayout<NM> WL(tg, ns);
     const size_t smem = WL.bytes;
     auto kern = sweep_ws_kernel<NM, C, 0>;
     if constexpr (NM == 5) {  // the profiled shape: static one-segment tiles
-      if (tg.span == 256) kern = sweep_ws_kernel<NM, C, 256 / C>;
+      if (tg.span == 256) kern = groups > 2 ? sweep_ws_kernel<NM, C, 256 / C, 3> : sweep_ws_kernel<NM, C, 256 / C>;
     }
+    if (groups > 2 && !(NM == 5 && tg.span == 256)) groups = 2;  // 3 groups: the profiled shape only
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return set_error(STRAIT_ECUDA, "strait_sweep: %zu B shared memory per CTA unavailable", smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);

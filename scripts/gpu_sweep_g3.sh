@@ -1,0 +1,6 @@
+# sweep pipeline shape with the 3-group (72-register) instantiation: stages x groups, then parity at the winner
+nvidia-smi -L
+for cfg in "2 1" "3 3" "4 3" "2 2" "4 2"; do set -- $cfg
+  STRAIT_SWEEP_STAGES=$1 STRAIT_SWEEP_GROUPS=$2 timeout 300 python bench.py --steps 300 --warmup 3 --no-replay --no-single --e2e-steps 1 --no-cpu-baseline --no-parity 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('ns=$1 gr=$2', round(r['kernel_ms'],4), round(r['frac'],3), d['clocks']['reasons'], d['clocks']['sm_mhz'])"
+done
+STRAIT_SWEEP_STAGES=4 STRAIT_SWEEP_GROUPS=3 timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_bench_parity_gpu.py -q -x -p no:cacheprovider -k "sweep or c3 or round" > gpurun_out/pytest_sweep.txt 2>&1; tail -3 gpurun_out/pytest_sweep.txt

@@ -139,12 +139,46 @@ def test_replay_c2_full_size_vs_oracle(cuda, oracle):
     assert np.all(s["b_kernel_start"] >= s["b_transfer_end"] - 1e-9)
 
 
+def test_replay_wide_geometry_vs_oracle(cuda, oracle):
+    """Concurrency limits up to 32 per GPU, and nodes past the one-warp
+    shared-memory budget (128 GPUs: one replay per CTA of 8 warps, traced and
+    untraced), against the oracle."""
+    from paper_2604_28175_b200 import config as MC
+    from paper_2604_28175_b200.replay import ReplayBatch, ReplaySpec
+
+    specs = [ReplaySpec(MC.config_from_dict(overload_doc(200, concurrency_limit=c, n_gpus=g)), c)
+             for c, g in ((9, 4), (12, 2), (32, 1))]
+    batch, res = device_run(specs)
+    res.check()
+    ores = oracle.replay(batch, threads=3)
+    for r in range(batch.R):
+        s, o = res.replay_slice(r), ores.replay_slice(r)
+        assert_categorical_equal(s, o, f"replay {r}")
+        for k in FLOAT_KEYS:
+            np.testing.assert_array_equal(s[k], o[k], err_msg=f"replay {r}: {k}")
+    # 128 GPUs x 4 slots; 76 GPUs x 8 slots (past the one-warp budget: CTA layout only)
+    for g, c in ((128, 4), (76, 8)):
+        big = [ReplaySpec(MC.config_from_dict(overload_doc(150, n_gpus=g, concurrency_limit=c)), 1)]
+        for trace in (False, True):
+            b = ReplayBatch(big, trace=trace)
+            rb = b.run()
+            rb.check()
+            s, o = rb.replay_slice(0), oracle.replay(b, threads=1).replay_slice(0)
+            assert_categorical_equal(s, o, f"{g} GPUs x {c} trace={trace}")
+            for k in FLOAT_KEYS:
+                np.testing.assert_array_equal(s[k], o[k], err_msg=f"{g} GPUs x {c} trace={trace}: {k}")
+
+
 def test_replay_rejects_unsupported_geometry(cuda):
+    """Past 32 running batches per GPU (one lane per list position), or past
+    the 227 KB a CTA can hold, the launch raises instead of running."""
     from paper_2604_28175_b200 import config as MC
     from paper_2604_28175_b200.replay import ReplaySpec
 
     with pytest.raises(ValueError):
-        device_run([ReplaySpec(MC.config_from_dict(overload_doc(100, concurrency_limit=9)))])
+        device_run([ReplaySpec(MC.config_from_dict(overload_doc(100, concurrency_limit=33)))])
+    with pytest.raises(ValueError):
+        device_run([ReplaySpec(MC.config_from_dict(overload_doc(100, n_gpus=1024)))])
 
 
 @pytest.mark.parametrize("name", CASES)
