@@ -107,6 +107,31 @@ struct Pred {
     bool s;
     return predict(a, cmp, mem, prio, s);
   }
+#if STRAIT_LIBM
+  // Two predictions for the same self terms and priority (a running entry's
+  // intf_cur and intf_new) as one straight-line block, so their dependent
+  // chains interleave.  Bit-identical to two predict() calls: the same
+  // operations in the same order; the inputs that need exp()'s special cases
+  // or the z > 500 saturation take predict() itself.
+  __device__ __forceinline__ void predict2(const double (&a1)[NM], const double (&a2)[NM], double cmp, double mem,
+                                           int prio, double& out1, double& out2) const {
+    const double x1 = exponent(a1, cmp, mem), x2 = exponent(a2, cmp, mem);
+    const double z1 = x1 * log_base, z2 = x2 * log_base;
+    bool special = z1 > kLogSaturate || z2 > kLogSaturate;
+    const double e1 = glibc::exp_common(z1, etab, special), e2 = glibc::exp_common(z2, etab, special);
+    if (special) {
+      out1 = predict(a1, cmp, mem, prio);
+      out2 = predict(a2, cmp, mem, prio);
+      return;
+    }
+    const double in1 = scale * e1 + offset, in2 = scale * e2 + offset;
+    const double f1 = in1 >= cap ? cap : py_min(py_max(in1, 0.0), cap);
+    const double f2 = in2 >= cap ? cap : py_min(py_max(in2, 0.0), cap);
+    const double cf = prio == 0 ? coeff[0] : coeff[1];
+    out1 = 1.0 + f1 * cf;
+    out2 = 1.0 + f2 * cf;
+  }
+#endif
 };
 
 // Runtime-NM dispatch: instantiate `F<NM>` for NM = 1..8.

@@ -80,6 +80,34 @@ __device__ __forceinline__ double exp_core(double x, double xtail, uint64_t sign
 
 __device__ __forceinline__ const ulonglong2* exp_table() { return reinterpret_cast<const ulonglong2*>(kExpTab); }
 
+// exp()'s common path with no branch: equal to exp(x) whenever x needs none of
+// its special cases (2^-54 <= |x| < 512), which is flagged in `special`
+// otherwise (the value is then meaningless and must be discarded).  Two calls
+// in one basic block interleave; callers recompute the rare special inputs.
+__device__ __forceinline__ double exp_common(double x, const ulonglong2* tab, bool& special) {
+  const uint32_t abstop = top12(x) & 0x7ff;
+  special |= abstop - 0x3c9u >= 0x408u - 0x3c9u;
+  constexpr double InvLn2N = kExpInvLn2N, Shift = kExpShift;
+  constexpr double NegLn2hiN = kExpNegLn2hiN, NegLn2loN = kExpNegLn2loN;
+  constexpr double C2 = kExpC2, C3 = kExpC3, C4 = kExpC4, C5 = kExpC5;
+  double kd = __fma_rn(x, InvLn2N, Shift);  // the exp_core<false> sequence, line for line
+  const uint64_t ki = as_u(kd);
+  kd -= Shift;
+  double r = __fma_rn(kd, NegLn2hiN, x);
+  r = __fma_rn(kd, NegLn2loN, r);
+  const uint64_t top = ki << (52 - kExpBits);
+  const ulonglong2 te = tab[ki % kN];
+  const double tail = as_d(te.x);
+  const uint64_t sbits = te.y + top;
+  const double r2 = r * r;
+  const double p23 = __fma_rn(r, C3, C2);
+  const double p45 = __fma_rn(r, C5, C4);
+  double tmp = __fma_rn(p23, r2, r + tail);
+  tmp = __fma_rn(p45, r2 * r2, tmp);
+  const double scale = as_d(sbits);
+  return __fma_rn(tmp, scale, scale);
+}
+
 // math.exp (e_exp.c __exp, FMA build)
 __device__ __forceinline__ double exp(double x, const ulonglong2* tab = exp_table()) {
   uint32_t abstop = top12(x) & 0x7ff;

@@ -304,9 +304,11 @@ struct Sim : Geom<GEOM> {
   __device__ __forceinline__ int slot_at(int g, int p) const { return slot(g, ORD(p, g)); }
 
   __device__ __forceinline__ void sync() const { __syncwarp(); }
-  // named barrier over the replay's NW warps (ids 1-3; 0 is __syncthreads)
+  // named barrier over the replay's NW warps (ids 1-3; 0 is __syncthreads).  The
+  // master and the helpers reach it from different code locations, so it is the
+  // non-.aligned form (bar.sync is barrier.sync.aligned).
   __device__ __forceinline__ void cta_bar(int id) const {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NT) : "memory");
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(NT) : "memory");
   }
   // master: the job fields were written by lane 0; wake the helpers
   __device__ __forceinline__ void post_job() const {
@@ -1471,9 +1473,6 @@ struct Sim : Geom<GEOM> {
     const int g = SI(SI_GPU, s), j = SI(SI_J, s);
     const int m = SB(SB_MODEL, s), k = SB(SB_SIZE, s), prio = SB(SB_PRIO, s);
     const int bid = SI(SI_BID, s), req0 = SI(SI_REQ0, s);
-    // the batch's (first 32) requests: global index and arrival time are loaded
-    // here and consumed after the bookkeeping below, which hides their latency
-    const int64_t g_pre = lane < k ? req_at(req0 + lane) : 0;
     bool ok = true;
     const double seg_d = now - SD(SD_LAST, s), seg_slow = SD(SD_SLOW, s);
     sync();
@@ -1481,22 +1480,16 @@ struct Sim : Geom<GEOM> {
     if (seg_d > 0) trace1(STRAIT_TR_SEGMENT, now, g, bid, -1, 0, seg_d, seg_slow);  // ExecutionState.finish
     fail_any(!ok, STRAIT_EORDER);
     sync();
-    const double a_pre = lane < k ? arr(g_pre) : 0.0;
     const double measured = now - SD(SD_KS, s);
     const double completion = now + (tab_total(m, k) - tab_transfer(m, k) - tab_kernel(m, k));
     const double dl = mdeadline(m);
-    double tw[NM];
-    tl_twa(s, now, tw);
-    const double tk = tab_kernel(m, k);
-    const double actual = MathT::div(measured, tk);
-    if (!(actual > 0)) fail(STRAIT_EINVAL);
     int nviol = 0;
     for (int i0 = 0; i0 < k; i0 += 32) {
       const int i = i0 + lane;
       bool viol = false;
       if (i < k) {
-        const int64_t gidx = i0 ? req_at(req0 + i) : g_pre;
-        viol = completion > (i0 ? arr(gidx) : a_pre) + dl;
+        const int64_t gidx = req_at(req0 + i);
+        viol = completion > arr(gidx) + dl;
         A->req_status[gidx] = 1;
         A->req_violated[gidx] = (uint8_t)viol;
         A->req_completion[gidx] = completion;
@@ -1507,6 +1500,11 @@ struct Sim : Geom<GEOM> {
     resolved += k;
     if (prio == 0) c_hp_viol += nviol;
     else c_lp_viol += nviol;
+    double tw[NM];
+    tl_twa(s, now, tw);
+    const double tk = tab_kernel(m, k);
+    const double actual = MathT::div(measured, tk);
+    if (!(actual > 0)) fail(STRAIT_EINVAL);
     // GpuRuntimeState.remove_entry (runtime.py:132-141): shift the running list
     const int n = GI(GI_NRUN, g);
     int pos = 0;

@@ -29,7 +29,10 @@ namespace strait {
 
 constexpr int kSweepThreads = 256;       // compute threads per CTA (one per triple)
 constexpr int kMaxStages = 4;
-constexpr int kMaxGroups = 3;  // consumer groups of 8 warps (named barriers 1 .. 15)
+constexpr int kMaxGroups = 2;  // consumer groups of 8 warps (named barriers 1 .. 10)
+// an upper bound of RN(cap / 100) for cap >= 0: RN(cap * kCapFractionHi) exceeds
+// cap / 100 by a relative ~2^-40, far above the two roundings (each <= 2^-53)
+constexpr double kCapFractionHi = 0.01 * (1.0 + 0x1p-40);
 
 // A *tile* is the unit one CTA processes at a time: `spb` consecutive segments
 // (all of their pairs and triples), contiguous in every SoA field array.
@@ -411,10 +414,8 @@ __device__ __forceinline__ int build_copy_table(const StraitSweepArgs& a, const 
 
 // SG != 0 fixes gpus_per_segment at compile time (SG * C == 256: one segment per
 // tile) so every shared-memory offset folds into an immediate.
-// MAXG = most consumer groups the instantiation runs: 2 (<= 113 registers, up to
-// 2 CTAs of one group per SM) or 3 (one CTA of 3 groups, <= 78 registers).
-template <int NM, int C, int SG, int MAXG = 2>
-__global__ void __launch_bounds__(32 * (8 * MAXG + 2), 1)
+template <int NM, int C, int SG>
+__global__ void __launch_bounds__(32 * (8 * kMaxGroups + 2), 1)
     sweep_ws_kernel(const StraitSweepArgs a, const StraitRefitArgs r, int with_refit, int nstages, int groups,
                     int diag, const __grid_constant__ CUtensorMap ent_map,
                     const __grid_constant__ CUtensorMap pair_map, int use_tmap) {
@@ -548,12 +549,17 @@ __global__ void __launch_bounds__(32 * (8 * MAXG + 2), 1)
     const int cprio = active ? ((const int8_t*)(stage + L.cprio))[4 * sl + (int)((tile * spb + sl) & 3)] : 0;
     const int eprio = active ? ((const int8_t*)(stage + L.eprio))[local] : 0;
     // check_violate answers True at the LOW candidate's AIMD-cap test before it
-    // reads any co-runner (scheduler.py:129-135): such pairs project nothing
+    // reads any co-runner (scheduler.py:129-135): such pairs project nothing.
+    // This test only skips work, so it may be conservative: it compares against
+    // an upper bound of cap_pct / 100 (one multiply, not a division on the path
+    // to the projection); the pair lanes below apply the exact test, and the
+    // pair's flag is the exact test OR the projections.
     bool capv = false;
     if (active && cprio == 1) {
-      const double cap_fraction = pair[(2 * NM) * TP + pl] / 100.0;
+      const double cap = pair[(2 * NM) * TP + pl];
+      const double cap_hi = cap >= 0.0 ? cap * kCapFractionHi : __longlong_as_double(0x7ff8000000000000LL);
 #pragma unroll
-      for (int m = 0; m < NM; ++m) capv |= pair[(NM + m) * TP + pl] + cand[m * spb + sl] > cap_fraction;
+      for (int m = 0; m < NM; ++m) capv |= pair[(NM + m) * TP + pl] + cand[m * spb + sl] > cap_hi;
     }
     bool viol = false;
     if (active && c < nrun && eprio <= cprio && !capv && !(diag & 8)) {  // diag 8: skip the projections (timing only)
@@ -562,13 +568,18 @@ __global__ void __launch_bounds__(32 * (8 * MAXG + 2), 1)
       for (int m = 0; m < NM; ++m) tw[m] = ent[(NM + m) * TT + local];
       const double cmp = ent[(2 * NM + 0) * TT + local], mem = ent[(2 * NM + 1) * TT + local];
       const double tk = ent[(2 * NM + 2) * TT + local], ks = ent[(2 * NM + 4) * TT + local];
-      const double intf_cur = pr.predict(tw, cmp, mem, eprio);
+#pragma unroll
+      for (int m = 0; m < NM; ++m) nagg[m] = pair[m * TP + pl] - ent[m * TT + local] + cand[m * spb + sl];
+      double intf_cur, intf_new;  // current progress under the TWA co-location; the candidate joining
+#if STRAIT_LIBM
+      pr.predict2(tw, nagg, cmp, mem, eprio, intf_cur, intf_new);
+#else
+      intf_cur = pr.predict(tw, cmp, mem, eprio);
+      intf_new = pr.predict(nagg, cmp, mem, eprio);
+#endif
       const double elapsed = py_max(0.0, now - ks);
       const double denom = intf_cur * tk;
       const double progress = denom > 0 ? py_min(1.0, elapsed / denom) : 1.0;
-#pragma unroll
-      for (int m = 0; m < NM; ++m) nagg[m] = pair[m * TP + pl] - ent[m * TT + local] + cand[m * spb + sl];
-      const double intf_new = pr.predict(nagg, cmp, mem, eprio);
       const double remaining = (1.0 - progress) * tk * intf_new;
       const double projected = py_max(now, ks) + remaining;
       viol = projected > ent[(2 * NM + 3) * TT + local];
@@ -592,57 +603,52 @@ __global__ void __launch_bounds__(32 * (8 * MAXG + 2), 1)
       if (lane == 0) mbar_arrive(&empty[st]);
       continue;
     }
-    asm volatile("bar.sync %0, %1;" ::"r"(bar1), "r"(8 * 32) : "memory");
 
     // ---- 2. pair: LP cap + check_meet, one lane per pair on the first ceil(TP/32) warps ----
-    // The pair lanes first copy what they still need out of the stage into
-    // registers and release it, so the producer refills it while the meet
-    // predictions and the argmin run (they only touch the stage's result area,
-    // which TMA never writes and which only these warps use, in tile order).
+    // Neither reads the projections, so the pair lanes run both BEFORE waiting
+    // for the tile's projections (the wait is then mostly hidden), then read the
+    // projections' violate bits and release the stage: the producer refills it
+    // while the argmin runs (it only touches the stage's result area, which TMA
+    // never writes and which only these warps use, in tile order).
     {
       const int pp = wg * 32 + lane;
       const bool pact = pp < TP;
       const int psl = pact ? pp / G : 0;
       int pn = 0, pprio = 0;
-      bool violate = false;
-      double agg[NM], cmp = 0.0, mem = 0.0, total = 0.0, kern = 0.0, front = 0.0, dline = 0.0, tav = 0.0;
+      bool capx = false, ok = false;
+      double lat = nan, intf = nan;
       if (pact) {
         pn = ((const int8_t*)(stage + L.nrun))[pp];
         pprio = ((const int8_t*)(stage + L.cprio))[4 * psl + (int)((tile * spb + psl) & 3)];
-        violate = s_viol[pp] != 0;
-        if (pprio == 1) {  // LOW candidate vs the AIMD cap (scheduler.py:130-135)
+        if (pprio == 1) {  // LOW candidate vs the AIMD cap (scheduler.py:130-135), exact
           const double cap_fraction = pair[(2 * NM) * TP + pp] / 100.0;  // runtime.py:39-40
 #pragma unroll
           for (int m = 0; m < NM; ++m)
-            if (pair[(NM + m) * TP + pp] + cand[m * spb + psl] > cap_fraction) violate = true;
+            if (pair[(NM + m) * TP + pp] + cand[m * spb + psl] > cap_fraction) capx = true;
         }
+        if (pn < a.concurrency_limit) {  // has_slot (runtime.py:101-102), then check_meet
+          double assumed[NM];  // half the GPU aggregate (scheduler.py:178)
 #pragma unroll
-        for (int m = 0; m < NM; ++m) agg[m] = pair[m * TP + pp];
-        tav = pair[(2 * NM + 1) * TP + pp];
-        cmp = cand[(NM + 0) * spb + psl];
-        mem = cand[(NM + 1) * spb + psl];
-        total = cand[(NM + 2) * spb + psl];
-        kern = cand[(NM + 3) * spb + psl];
-        front = cand[(NM + 4) * spb + psl];
-        dline = cand[(NM + 5) * spb + psl];
+          for (int m = 0; m < NM; ++m) assumed[m] = 0.5 * pair[m * TP + pp];
+          const double cmp = cand[(NM + 0) * spb + psl], mem = cand[(NM + 1) * spb + psl];
+          intf = (diag & 16) ? assumed[0]  // diag 16: skip check_meet's prediction (timing only)
+                             : pr.predict(assumed, cmp, mem, pprio);
+          const double wait = py_max(0.0, pair[(2 * NM + 1) * TP + pp] - now);  // pcie.py:21-23
+          lat = cand[(NM + 2) * spb + psl] + wait + (intf - 1.0) * cand[(NM + 3) * spb + psl] +
+                (now - cand[(NM + 4) * spb + psl]);
+          ok = lat <= cand[(NM + 5) * spb + psl];
+        }
       }
+      asm volatile("bar.sync %0, %1;" ::"r"(bar1), "r"(8 * 32) : "memory");  // the tile's projections
+      const bool violate = pact && (capx || s_viol[pp] != 0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);  // the TMA region of this stage is free
       if (pact) {
         uint8_t flags = 0;
-        double lat = nan, intf = nan;
         bool admitted = false;
-        if (pn < a.concurrency_limit) {  // has_slot (runtime.py:101-102)
+        if (pn < a.concurrency_limit) {
           flags |= STRAIT_PAIR_HAS_SLOT;
           if (violate) flags |= STRAIT_PAIR_VIOLATE;
-          double assumed[NM];  // check_meet: half the GPU aggregate (scheduler.py:178)
-#pragma unroll
-          for (int m = 0; m < NM; ++m) assumed[m] = 0.5 * agg[m];
-          intf = (diag & 16) ? assumed[0]  // diag 16: skip check_meet's prediction (timing only)
-                             : pr.predict(assumed, cmp, mem, pprio);
-          const double wait = py_max(0.0, tav - now);  // pcie.py:21-23
-          lat = total + wait + (intf - 1.0) * kern + (now - front);
-          const bool ok = lat <= dline;
           if (ok) flags |= STRAIT_PAIR_MEET;
           admitted = !(a.use_violate && violate) && !(a.use_meet && !ok);
           if (admitted) flags |= STRAIT_PAIR_FEASIBLE;
@@ -861,16 +867,14 @@ static int launch_sweep_c(const StraitSweepArgs& a, cudaStream_t st, const Strai
   if (use_tma) {
     int groups = env_int("STRAIT_SWEEP_GROUPS", 1);
     groups = groups < 1 ? 1 : (groups > kMaxGroups ? kMaxGroups : groups);
-    int ns = env_int("STRAIT_SWEEP_STAGES", groups > 2 ? 4 : 2);
+    int ns = env_int("STRAIT_SWEEP_STAGES", 2);
     ns = ns < 2 ? 2 : (ns > kWsMaxStages ? kWsMaxStages : ns);
-    if (ns < groups) ns = groups;  // every group owns a stage in flight
     const WsLayout<NM> WL(tg, ns);
     const size_t smem = WL.bytes;
     auto kern = sweep_ws_kernel<NM, C, 0>;
     if constexpr (NM == 5) {  // the profiled shape: static one-segment tiles
-      if (tg.span == 256) kern = groups > 2 ? sweep_ws_kernel<NM, C, 256 / C, 3> : sweep_ws_kernel<NM, C, 256 / C>;
+      if (tg.span == 256) kern = sweep_ws_kernel<NM, C, 256 / C>;
     }
-    if (groups > 2 && !(NM == 5 && tg.span == 256)) groups = 2;  // 3 groups: the profiled shape only
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return set_error(STRAIT_ECUDA, "strait_sweep: %zu B shared memory per CTA unavailable", smem);
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
