@@ -44,6 +44,7 @@ __host__ __device__ __forceinline__ double py_min(double a, double b) { return (
 // Transcendental policy of the predictor: inlined (default), or routed by a
 // kernel to shared out-of-line copies (MathT with the same static members).
 struct InlineMath {
+  static constexpr bool kInline = true;  // exp is inlined: two effects may interleave (Pred::effect2)
   static __device__ __forceinline__ double exp(double x, const ulonglong2* tab) { return dexp(x, tab); }
   static __device__ __forceinline__ double log(double x) { return dlog(x); }
 };
@@ -106,6 +107,27 @@ struct Pred {
                                             int prio) const {
     bool s;
     return predict(a, cmp, mem, prio, s);
+  }
+  // Two kernel_effect()s as one block, so their exp chains interleave when exp
+  // is inlined (bit-identical to two effect() calls; the inputs that need the
+  // saturation or exp()'s special cases take effect() itself).
+  __device__ __forceinline__ void effect2(double x1, double x2, double& e1, double& e2) const {
+#if STRAIT_LIBM
+    if constexpr (MathT::kInline) {
+      const double z1 = x1 * log_base, z2 = x2 * log_base;
+      bool special = z1 > kLogSaturate || z2 > kLogSaturate;
+      const double p1 = glibc::exp_common(z1, etab, special), p2 = glibc::exp_common(z2, etab, special);
+      if (!special) {
+        const double in1 = scale * p1 + offset, in2 = scale * p2 + offset;
+        e1 = in1 >= cap ? cap : py_min(py_max(in1, 0.0), cap);
+        e2 = in2 >= cap ? cap : py_min(py_max(in2, 0.0), cap);
+        return;
+      }
+    }
+#endif
+    bool s;
+    e1 = effect(x1, s);
+    e2 = effect(x2, s);
   }
 #if STRAIT_LIBM
   // Two predictions for the same self terms and priority (a running entry's

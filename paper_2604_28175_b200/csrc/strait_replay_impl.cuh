@@ -61,7 +61,7 @@ namespace rp {
 enum { RPF_SELECT, RPF_ARRIVAL, RPF_RANK, RPF_DROP, RPF_ELIG, RPF_PROPOSE, RPF_SUBMIT, RPF_ICUR, RPF_TIMEOUTS,
        RPF_TC, RPF_KC_PRE, RPF_KC_UPDATE, RPF_KC_POST, RPF_TICK, RPF_POST, RPF_TOTAL,
        RPF_N_QUEUES, RPF_N_ELIGIBLE, RPF_N_PROPOSE_WIDE, RPF_N_SUBMIT, RPF_N_ICUR_ALL, RPF_SUM_KMAX, RPF_N_NOSLOT,
-       RPF_SUM_ENTRIES, RPF_CTA_A, RPF_CTA_B, RPF_CTA_M, RPF_N_CTA, RPF_N };
+       RPF_SUM_ENTRIES, RPF_CTA_A, RPF_CTA_B, RPF_CTA_M, RPF_N_CTA, RPF_CTA_PA, RPF_CTA_PB, RPF_CTA_J, RPF_N };
 #define RP_CNT(i) (++prof[i])
 extern __device__ unsigned long long g_replay_prof[RPF_N];
 #define RP_T(v) const long long v = clock64()
@@ -83,6 +83,7 @@ static __device__ __noinline__ double rp_pow(double x, double y) { return dpow(x
 static __device__ __noinline__ double rp_div(double a, double b) { return __ddiv_rn(a, b); }
 
 struct OutlineMath {
+  static constexpr bool kInline = false;
   static __device__ __forceinline__ double exp(double x, const ulonglong2*) { return rp_exp(x); }
   static __device__ __forceinline__ double log(double x) { return rp_log(x); }
   static __device__ __forceinline__ double pow(double x, double y) { return rp_pow(x, y); }
@@ -238,7 +239,11 @@ struct Geom<3> {
 // the NW - 1 helper warps, parked on named barrier 1, join it.  Every job reads
 // the replay state and writes only per-item scratch (or per-slot caches that
 // no other item touches); barrier 2 ends it.  Same arithmetic, same bits.
-template <int NM, typename MathT, bool TR, bool LEAN, int GEOM, int NW = 1>
+// ILP: eval_pair evaluates check_meet and the co-runner projections two exp
+// chains at a time (Pred::effect2) — the lower latency for single replays; a
+// launch with several replays per SM keeps the smaller one-chain code, which
+// the instruction cache rewards there.
+template <int NM, typename MathT, bool TR, bool LEAN, int GEOM, int NW = 1, bool ILP = true>
 struct Sim : Geom<GEOM> {
   using Geom<GEOM>::G;
   using Geom<GEOM>::C;
@@ -780,15 +785,61 @@ struct Sim : Geom<GEOM> {
     return SD(SD_ST, s) + SD(SD_RB, s) * intf_new;
   }
 
-  // one (size, GPU) pair of best_for (scheduler.py:263-280): has_slot, violate, meet
+  // pressure_exponent of (agg - e.contrib) + add for co-runner s (scheduler.py:150-153)
+  __device__ __forceinline__ double proj_x(int s, const Cand& cd) const {
+    double x = SD(SD_X0, s);  // self terms first (cached with intf_cur)
+#pragma unroll
+    for (int i = 0; i < NM; ++i) x += pr.w[i] * (SD(SD_AEX + i, s) + cd.c[i]);
+    return x;
+  }
+  // max(now, ks) + ((1 - progress) * t_kernel) * intf_new > deadline (scheduler.py:154-160)
+  __device__ __forceinline__ bool proj_late(int s, double eff, int ep) const {
+    const double intf_new = 1.0 + eff * (ep == 0 ? pr.coeff[0] : pr.coeff[1]);
+    return SD(SD_ST, s) + SD(SD_RB, s) * intf_new > SD(SD_DL, s);
+  }
+
+  // one (size, GPU) pair of best_for (scheduler.py:263-280): has_slot, violate, meet.
+  // With exp inlined, check_meet's prediction and the co-runner projections are
+  // evaluated two chains at a time ((meet, c0), (c1, c2), (c3, -), ...), stopping
+  // at the first violating pair of chains: check_violate's boolean and the meet
+  // are pure, so the result is the sequential one.
   __device__ __forceinline__ bool eval_pair(int g, const Cand& cd, int cprio, double dl, double front, double now,
                                             double& lat, double& intf) const {
-    if (!(GI(GI_NRUN, g) < CONC)) return false;  // has_slot (runtime.py:101-102)
-    if (cf->use_violate && violate(g, cd, cprio, now)) return false;
+    const int n = GI(GI_NRUN, g);
+    if (!(n < CONC)) return false;  // has_slot (runtime.py:101-102)
     double assumed[NM];  // check_meet (scheduler.py:164-185): half the aggregate
 #pragma unroll
     for (int i = 0; i < NM; ++i) assumed[i] = 0.5 * GD(GD_AGG + i, g);
-    intf = pr.predict(assumed, cd.cmp, cd.mem, cprio);
+    if constexpr (MathT::kInline && ILP) {
+      if (cf->use_violate && cprio == 1) {  // LOW: LP aggregate + contribution vs the AIMD cap (:130-135)
+        const double capf = GD(GD_CAPF, g);
+#pragma unroll
+        for (int i = 0; i < NM; ++i)
+          if (GD(GD_LPA + i, g) + cd.c[i] > capf) return false;
+      }
+      const bool uv = cf->use_violate;
+      if (n == 0) {
+        intf = pr.predict(assumed, cd.cmp, cd.mem, cprio);
+      } else {  // (meet, co-runner 0)
+        const int s0 = slot_at(g, 0);
+        const int ep0 = SB(SB_PRIO, s0);
+        double em, e0;
+        pr.effect2(pr.exponent(assumed, cd.cmp, cd.mem), proj_x(s0, cd), em, e0);
+        intf = 1.0 + em * (cprio == 0 ? pr.coeff[0] : pr.coeff[1]);
+        if (uv && ep0 <= cprio && proj_late(s0, e0, ep0)) return false;
+      }
+      for (int p = 1; p < n; p += 2) {  // (c1, c2), (c3, c4), ...
+        const int sa = slot_at(g, p), sb = p + 1 < n ? slot_at(g, p + 1) : sa;
+        const int ea = SB(SB_PRIO, sa), eb = SB(SB_PRIO, sb);
+        double fa, fb;
+        pr.effect2(proj_x(sa, cd), proj_x(sb, cd), fa, fb);
+        if (uv && ((ea <= cprio && proj_late(sa, fa, ea)) || (p + 1 < n && eb <= cprio && proj_late(sb, fb, eb))))
+          return false;
+      }
+    } else {
+      if (cf->use_violate && violate(g, cd, cprio, now)) return false;
+      intf = pr.predict(assumed, cd.cmp, cd.mem, cprio);
+    }
     lat = cd.total + py_max(0.0, GD(GD_TAV, g) - now) + (intf - 1.0) * cd.kern + (now - front);
     return !(cf->use_meet && !(lat <= dl));
   }
@@ -903,54 +954,74 @@ struct Sim : Geom<GEOM> {
                                               double now) const {
     const int C1 = CONC + 1;
     const int t = w * 32 + lane;
-    // A1. projections, items (k, g, c) from thread 0 up; the warps stay on one path
-    if (cf->use_violate) {
-      const int ni = kmax * NG * CONC;
-      for (int i = t; i < ni; i += NT) {
-        const int pg = i / CONC, c = i - pg * CONC;
-        const int kq = pg / NG, g = pg - kq * NG;
-        const int n = GI(GI_NRUN, g);
-        if (!(n < CONC)) continue;  // has_slot fails: phase B never reads this pair's items
-        bool v = false;
-        if (c < n) {
-          const int s = slot_at(g, c);
-          const int ep = SB(SB_PRIO, s);
-          if (ep <= cprio) {
-            Cand cd;
-#pragma unroll
-            for (int q = 0; q < NM; ++q) cd.c[q] = thr(m, k0 + kq + 1, q);
-            v = projection(s, cd, ep) > SD(SD_DL, s);
-          }
-        }
-        pv[pg * C1 + c] = v;
-      }
-    }
-    // A2. the pairs' LP-cap test + check_meet, items (k, g) from the last thread
-    // down, so that they fall on threads with no (or the fewest) projections
+    // Phase A in rounds of NT: thread t takes projection item r0 + t (items
+    // (k, g, c), from thread 0 up) and meet item r0 + NT - 1 - t (items (k, g),
+    // from the last thread down), and evaluates both effects as one block
+    // (Pred::effect2, the exp chains interleave); an absent item computes a
+    // dummy exponent whose result is discarded, so the warps stay on one path.
+    RP_T(t_pa);
+    const bool uv = cf->use_violate;
+    const int ni = uv ? kmax * NG * CONC : 0;
     const int np2 = kmax * NG;
-    for (int pg = NT - 1 - t; pg < np2; pg += NT) {
-      const int kq = pg / NG, g = pg - kq * NG;
-      if (!(GI(GI_NRUN, g) < CONC)) continue;
-      Cand cd;
-      load_cand(m, k0 + kq + 1, cd);
-      bool capv = false;
-      if (cprio == 1) {
-        const double capf = GD(GD_CAPF, g);
+    for (int r0 = 0; r0 < ni || r0 < np2; r0 += NT) {  // warp-uniform trip count
+      const int i = r0 + t, pg2 = r0 + NT - 1 - t;
+      bool hp = false, hm = false;
+      int s = 0, ep = 0, pgi = 0, ci = 0, g2 = 0;
+      double xp = 1.0, xm = 1.0;
+      if (i < ni) {  // A1: check_violate's projection of running entry ci of GPU g (scheduler.py:137-160)
+        pgi = i / CONC, ci = i - pgi * CONC;
+        const int kq = pgi / NG, g = pgi - kq * NG;
+        const int n = GI(GI_NRUN, g);
+        if (n < CONC) {  // else has_slot fails: phase B never reads this pair's items
+          if (ci < n) {
+            s = slot_at(g, ci);
+            ep = SB(SB_PRIO, s);
+            if (ep <= cprio) {
+              Cand cd;
 #pragma unroll
-        for (int q = 0; q < NM; ++q) capv |= GD(GD_LPA + q, g) + cd.c[q] > capf;
+              for (int q = 0; q < NM; ++q) cd.c[q] = thr(m, k0 + kq + 1, q);
+              xp = proj_x(s, cd);
+              hp = true;
+            }
+          }
+          if (!hp) pv[pgi * C1 + ci] = 0;
+        }
       }
-      double assumed[NM];
+      Cand cm;
+      bool capv = false;
+      if (pg2 >= 0 && pg2 < np2) {  // A2: the pair's LP-cap test (:130-135) and check_meet (:164-185)
+        const int kq = pg2 / NG;
+        g2 = pg2 - kq * NG;
+        if (GI(GI_NRUN, g2) < CONC) {
+          load_cand(m, k0 + kq + 1, cm);
+          if (cprio == 1) {
+            const double capf = GD(GD_CAPF, g2);
 #pragma unroll
-      for (int q = 0; q < NM; ++q) assumed[q] = 0.5 * GD(GD_AGG + q, g);
-      const double intf = pr.predict(assumed, cd.cmp, cd.mem, cprio);
-      const double lat = cd.total + py_max(0.0, GD(GD_TAV, g) - now) + (intf - 1.0) * cd.kern + (now - front);
-      pm[pg] = (uint8_t)((lat <= dl ? 1 : 0) | (capv ? 2 : 0));
-      plat[pg] = lat;
-      pintf[pg] = intf;
+            for (int q = 0; q < NM; ++q) capv |= GD(GD_LPA + q, g2) + cm.c[q] > capf;
+          }
+          double assumed[NM];
+#pragma unroll
+          for (int q = 0; q < NM; ++q) assumed[q] = 0.5 * GD(GD_AGG + q, g2);
+          xm = pr.exponent(assumed, cm.cmp, cm.mem);
+          hm = true;
+        }
+      }
+      double fp, fm;
+      pr.effect2(xp, xm, fp, fm);
+      if (hp) pv[pgi * C1 + ci] = proj_late(s, fp, ep);
+      if (hm) {
+        const double intf = 1.0 + fm * (cprio == 0 ? pr.coeff[0] : pr.coeff[1]);
+        const double lat = cm.total + py_max(0.0, GD(GD_TAV, g2) - now) + (intf - 1.0) * cm.kern + (now - front);
+        pm[pg2] = (uint8_t)((lat <= dl ? 1 : 0) | (capv ? 2 : 0));
+        plat[pg2] = lat;
+        pintf[pg2] = intf;
+      }
     }
+    if (w == 0) RP_ADD(RPF_CTA_PA, t_pa);  // the master's own phase-A items
     RP_T(t_b);
     cta_bar(3);
     if (w == 0) RP_ADD(RPF_CTA_B, t_b);  // the master's wait at the end of phase A
+    RP_T(t_pb);
     const int lw = NG <= 1 ? 0 : 32 - __clz(NG - 1);
     const int W = 1 << lw, seg = W < 32 ? W : 32, nch = Layout::cta_chunks(NG);
     const int np = kmax << lw;
@@ -985,7 +1056,10 @@ struct Sim : Geom<GEOM> {
       }
       if ((lane & (seg - 1)) == 0 && kq < kmax) part[kq * nch + (g >> 5)] = Part{bl, bi, 0ull, found ? bg : -1, 0};
     }
+    if (w == 0) RP_ADD(RPF_CTA_PB, t_pb);  // the master's phase-B pairs
+    RP_T(t_j);
     cta_bar(2);
+    if (w == 0) RP_ADD(RPF_CTA_J, t_j);  // the master's wait at the join
   }
   // master side of JOB_PROPOSE: post it for sizes k0 + 1 .. k0 + kcnt and take part in it
   __device__ __forceinline__ void run_propose_job(int m, int k0, int kcnt, int cprio, double dl, double front,
@@ -1829,7 +1903,7 @@ struct Sim : Geom<GEOM> {
 // for 16 resident replays per SM (throughput: replay sweeps).
 // NW = 1: up to wpc replays per CTA, one warp each.  NW > 1: one replay per
 // CTA of NW warps (warp 0 the master, the others helpers).
-template <int NM, int MINB, bool TR, bool LEAN, int GEOM, int NW>
+template <int NM, int MINB, bool TR, bool LEAN, int GEOM, int NW, bool ILP = true>
 __global__ void __launch_bounds__(NW > 1 ? 32 * NW : 128, MINB)
     replay_kernel(const __grid_constant__ StraitReplayArgs a, int wpc) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1839,7 +1913,7 @@ __global__ void __launch_bounds__(NW > 1 ? 32 * NW : 128, MINB)
   const int64_t r = a.order ? (int64_t)a.order[slot_w] : slot_w;
   const Layout L(a.max_gpus, a.max_concurrency, a.models.n_models, NM, NW, a.models.stride);
   unsigned char* base = NW > 1 ? smem : smem + (size_t)w * L.bytes;
-  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type, TR, LEAN, GEOM, NW> S;
+  Sim<NM, typename std::conditional<(MINB >= 4), OutlineMath, FullInlineMath>::type, TR, LEAN, GEOM, NW, ILP> S;
   S.A = &a;
   S.cf = a.cfg + r;
   S.lane = threadIdx.x & 31;
@@ -1913,6 +1987,17 @@ inline bool c5_geometry(const StraitReplayArgs& a) {
 // latency variant
 constexpr int kCtaWarps = 8;
 
+inline int sm_count_cached() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
 template <int NM>
 int launch_replay(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb);
 
@@ -1923,10 +2008,10 @@ inline size_t cta_replay_smem(const StraitReplayArgs& a) {
   return b <= 227 * 1024 ? b : 0;
 }
 
-template <int NM, int MINB, bool TR, bool LEAN, int GEOM, int NW = 1>
+template <int NM, int MINB, bool TR, bool LEAN, int GEOM, int NW = 1, bool ILP = true>
 int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp) {
   const size_t smem = NW > 1 ? cta_replay_smem(a) : smem_per_warp * wpc;
-  auto* k = replay_kernel<NM, MINB, TR, LEAN, GEOM, NW>;
+  auto* k = replay_kernel<NM, MINB, TR, LEAN, GEOM, NW, ILP>;
   if (!smem || cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return set_error(STRAIT_ECUDA, "strait_replay: cannot reserve %zu B of shared memory", smem);
   const unsigned grid = NW > 1 ? (unsigned)a.n_replays : (unsigned)((a.n_replays + wpc - 1) / wpc);
@@ -1958,7 +2043,7 @@ int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_
     if constexpr (NMV == 5)                                                                                       \
       if (po && overload_geometry(a))                                                                             \
         return minb >= 4 ? launch_replay_occ<NMV, 4, false, true, 1>(a, st, wpc, smem_per_warp)                  \
-                         : a.models.stride == 8 ? launch_replay_occ<NMV, 1, false, true, 2>(a, st, wpc, smem_per_warp) \
+                         : a.models.stride == 8 ? (a.n_replays > sm_count_cached() ? launch_replay_occ<NMV, 1, false, true, 2, 1, false>(a, st, wpc, smem_per_warp) : launch_replay_occ<NMV, 1, false, true, 2>(a, st, wpc, smem_per_warp)) \
                                                 : launch_replay_occ<NMV, 1, false, true, 1>(a, st, wpc, smem_per_warp); \
     if (minb >= 4)                                                                                                \
       return po ? launch_replay_occ<NMV, 4, false, true, 0>(a, st, wpc, smem_per_warp)                           \

@@ -32,7 +32,7 @@ def main():
     lib.strait_replay_profile.restype = C.c_int
     for name, cfg in cases:
         b = ReplayBatch([ReplaySpec(cfg)])
-        out = np.zeros(28, np.uint64)
+        out = np.zeros(31, np.uint64)
         lib.strait_replay_profile(out.ctypes.data)  # reset
         res = b.run(metrics=False)
         lib.strait_replay_profile(out.ctypes.data)
@@ -51,7 +51,8 @@ def main():
         nc = max(int(out[27]), 1)
         if out[27]:
             print(f"  CTA proposes {out[27]}: post..join {out[24] / nc:.0f} cyc (master wait at phase A end "
-                  f"{out[25] / nc:.0f}), master combine {out[26] / nc:.0f} cyc")
+                  f"{out[25] / nc:.0f}), master combine {out[26] / nc:.0f} cyc; master phase A {out[28] / nc:.0f}, "
+                  f"phase B {out[29] / nc:.0f}, join wait {out[30] / nc:.0f}")
         w = max(int(out[18]), 1)
         print(f"  per wide propose: mean kmax {out[21] / w:.2f}, no GPU with a slot {100 * out[22] / w:.1f}%, "
               f"running entries {out[23] / w:.2f}")
