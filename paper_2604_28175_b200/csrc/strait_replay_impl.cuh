@@ -106,7 +106,7 @@ constexpr unsigned kFull = 0xffffffffu;
 __host__ __device__ __forceinline__ size_t al(size_t x) { return (x + 15) & ~(size_t)15; }
 
 // Shared-memory layout of one replay (one warp), grouped field arrays so the
-// engine needs only a handful of base pointers.  Slot s = j * G + g is
+// engine needs only a handful of base pointers.  Slot s = g * C + j is
 // running-batch slot j of GPU g (G, C = the launch's maximum geometry);
 // per-GPU fields are [field][G] so lanes over GPUs touch consecutive words.
 // Slot double fields (SD_*), then four NM-vectors: timeline value, timeline
@@ -115,7 +115,7 @@ __host__ __device__ __forceinline__ size_t al(size_t x) { return (x + 15) & ~(si
 // refreshed with intf_cur (icur_slot)
 enum { SD_DL, SD_KS, SD_T0, SD_TL, SD_REM, SD_SLOW, SD_NOISE, SD_LAST, SD_WORK, SD_RB, SD_X0, SD_ST, SD_CMP, SD_MEM,
        SD_TK, SD_VL };
-enum { SI_BID, SI_REQ0, SI_GPU, SI_J, SI_N };  // SI_GPU / SI_J: s % G and s / G, precomputed
+enum { SI_BID, SI_REQ0, SI_GPU, SI_J, SI_N };  // SI_GPU / SI_J: s / C and s % C, precomputed
 enum { SB_MODEL, SB_SIZE, SB_PRIO, SB_STARTED, SB_LIVE, SB_TLEN, SB_N };
 // GD_CAPF = cap_fraction() = cap_pct / 100 (runtime.py:39-40), refreshed wherever the cap changes
 enum { GD_TAV, GD_CAP, GD_TICK, GD_CAPF, GD_AGG };  // then NM aggregates, NM LP aggregates, C pending reservations
@@ -305,7 +305,10 @@ struct Sim : Geom<GEOM> {
   __device__ __forceinline__ int& GI(int f, int g) const { return gi[f * G + g]; }
   __device__ __forceinline__ int& QI(int f, int m) const { return qi[f * M + m]; }
   __device__ __forceinline__ int8_t& ORD(int p, int g) const { return go[p * G + g]; }
-  __device__ __forceinline__ int slot(int g, int j) const { return j * G + g; }
+  // GPU-major: a GPU's running batches are adjacent words, so lanes over one GPU's
+  // list positions (recompute, restamp, intf_cur) and the CTA's (GPU, co-runner)
+  // items read distinct shared-memory banks
+  __device__ __forceinline__ int slot(int g, int j) const { return g * C + j; }
   __device__ __forceinline__ int slot_at(int g, int p) const { return slot(g, ORD(p, g)); }
 
   __device__ __forceinline__ void sync() const { __syncwarp(); }
@@ -1723,8 +1726,8 @@ struct Sim : Geom<GEOM> {
     }
     for (int s = lane; s < S; s += 32) {
       SB(SB_LIVE, s) = 0;
-      SI(SI_GPU, s) = s % G;
-      SI(SI_J, s) = s / G;
+      SI(SI_GPU, s) = s / C;
+      SI(SI_J, s) = s % C;
     }
     for (int i = lane; i < NE; i += 32) {
       ed[i] = INF;
