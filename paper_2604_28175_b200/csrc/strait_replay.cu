@@ -121,8 +121,18 @@ extern "C" int strait_replay(const StraitReplayArgs* a, void* stream) {
 namespace strait {
 namespace rp {
 __device__ unsigned long long g_replay_prof[RPF_N];
+__device__ unsigned long long g_cta_warp[3][16];
 }  // namespace rp
 }  // namespace strait
+/* diagnostic build only: per-warp CTA propose-job timestamps (wake, phase-A end, phase-B end) summed */
+extern "C" int strait_replay_cta_profile(unsigned long long* out) {
+  using namespace strait::rp;
+  unsigned long long zero[48] = {};
+  if (cudaMemcpyFromSymbol(out, g_cta_warp, sizeof zero) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_cta_warp, zero, sizeof zero) != cudaSuccess)
+    return strait::set_error(STRAIT_ECUDA, "strait_replay_cta_profile: copy failed");
+  return 48;
+}
 /* diagnostic build only: accumulated engine cycles per phase since the last call (then reset) */
 extern "C" int strait_replay_profile(unsigned long long* out) {
   using namespace strait::rp;

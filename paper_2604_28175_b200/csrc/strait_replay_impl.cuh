@@ -64,6 +64,7 @@ enum { RPF_SELECT, RPF_ARRIVAL, RPF_RANK, RPF_DROP, RPF_ELIG, RPF_PROPOSE, RPF_S
        RPF_SUM_ENTRIES, RPF_CTA_A, RPF_CTA_B, RPF_CTA_M, RPF_N_CTA, RPF_CTA_PA, RPF_CTA_PB, RPF_CTA_J, RPF_N };
 #define RP_CNT(i) (++prof[i])
 extern __device__ unsigned long long g_replay_prof[RPF_N];
+extern __device__ unsigned long long g_cta_warp[3][16];  // per warp: wake, phase-A end, phase-B end (- post)
 #define RP_T(v) const long long v = clock64()
 #define RP_ADD(i, v) (prof[i] += clock64() - (v))
 #else
@@ -128,6 +129,7 @@ enum { JOB_EXIT, JOB_ICUR, JOB_PROPOSE, JOB_SELECT };
 struct Job {
   int kind, m, kmax, cprio, k0, pad;
   double now, dl, front;
+  long long t0;  // profiling build: the master's clock at the post
 };
 // one warp's partial of a reduction: an event-home minimum, or a size's best GPU
 struct Part {
@@ -941,6 +943,10 @@ struct Sim : Geom<GEOM> {
     return size;
   }
 
+  // (Measured and reverted: the jobs as out-of-line calls, so master and helpers
+  // share one copy of the code — call-boundary spills doubled a job's time; and
+  // the exp table in shared memory — no change, its lookups already hit L1.)
+  //
   // JOB_PROPOSE (every warp of the CTA): PredictivePolicy.propose's whole
   // (size x GPU x co-runner) search for queue m.
   //  A. items (k, g, c): c < CONC is check_violate's projection of running entry
@@ -1021,6 +1027,12 @@ struct Sim : Geom<GEOM> {
       }
     }
     if (w == 0) RP_ADD(RPF_CTA_PA, t_pa);  // the master's own phase-A items
+#if STRAIT_REPLAY_PROFILE
+    if (lane == 0) {
+      atomicAdd(&g_cta_warp[0][w], (unsigned long long)(t_pa - jb->t0));
+      atomicAdd(&g_cta_warp[1][w], (unsigned long long)(clock64() - jb->t0));
+    }
+#endif
     RP_T(t_b);
     cta_bar(3);
     if (w == 0) RP_ADD(RPF_CTA_B, t_b);  // the master's wait at the end of phase A
@@ -1060,6 +1072,9 @@ struct Sim : Geom<GEOM> {
       if ((lane & (seg - 1)) == 0 && kq < kmax) part[kq * nch + (g >> 5)] = Part{bl, bi, 0ull, found ? bg : -1, 0};
     }
     if (w == 0) RP_ADD(RPF_CTA_PB, t_pb);  // the master's phase-B pairs
+#if STRAIT_REPLAY_PROFILE
+    if (lane == 0) atomicAdd(&g_cta_warp[2][w], (unsigned long long)(clock64() - jb->t0));
+#endif
     RP_T(t_j);
     cta_bar(2);
     if (w == 0) RP_ADD(RPF_CTA_J, t_j);  // the master's wait at the join
@@ -1067,7 +1082,11 @@ struct Sim : Geom<GEOM> {
   // master side of JOB_PROPOSE: post it for sizes k0 + 1 .. k0 + kcnt and take part in it
   __device__ __forceinline__ void run_propose_job(int m, int k0, int kcnt, int cprio, double dl, double front,
                                                   double now) {
-    if (lane == 0) *jb = Job{JOB_PROPOSE, m, kcnt, cprio, k0, 0, now, dl, front};
+#if STRAIT_REPLAY_PROFILE
+    if (lane == 0) *jb = Job{JOB_PROPOSE, m, kcnt, cprio, k0, 0, now, dl, front, clock64()};
+#else
+    if (lane == 0) *jb = Job{JOB_PROPOSE, m, kcnt, cprio, k0, 0, now, dl, front, 0};
+#endif
     RP_T(t_a);
     post_job();
     job_propose(m, k0, kcnt, cprio, dl, front, now);

@@ -30,10 +30,12 @@ def main():
         cases.append((f"c5 {sys.argv[3]} ms (64 GPUs, 20 models)", c5(float(sys.argv[3]))))
     lib = D.lib()
     lib.strait_replay_profile.restype = C.c_int
+    cw = np.zeros(48, np.uint64)
     for name, cfg in cases:
         b = ReplayBatch([ReplaySpec(cfg)])
         out = np.zeros(31, np.uint64)
         lib.strait_replay_profile(out.ctypes.data)  # reset
+        lib.strait_replay_cta_profile(cw.ctypes.data)
         res = b.run(metrics=False)
         lib.strait_replay_profile(out.ctypes.data)
         c = res.counters[0]
@@ -49,7 +51,12 @@ def main():
         print(f"  per pass: queues visited {out[16] / p:.2f}, eligible {out[17] / p:.2f}, wide proposes "
               f"{out[18] / p:.2f}, submits {out[19] / p:.2f}, icur_all {out[20] / p:.2f}")
         nc = max(int(out[27]), 1)
+        lib.strait_replay_cta_profile(cw.ctypes.data)
         if out[27]:
+            w = cw.reshape(3, 16)[:, :8] / max(int(out[27]), 1)
+            print("  CTA propose job, per warp (cycles after the post): wake " + " ".join(f"{v:.0f}" for v in w[0]) +
+                  " | phase A end " + " ".join(f"{v:.0f}" for v in w[1]) + " | phase B end " +
+                  " ".join(f"{v:.0f}" for v in w[2]))
             print(f"  CTA proposes {out[27]}: post..join {out[24] / nc:.0f} cyc (master wait at phase A end "
                   f"{out[25] / nc:.0f}), master combine {out[26] / nc:.0f} cyc; master phase A {out[28] / nc:.0f}, "
                   f"phase B {out[29] / nc:.0f}, join wait {out[30] / nc:.0f}")
