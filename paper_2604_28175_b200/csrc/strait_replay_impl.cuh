@@ -1,7 +1,9 @@
 // strait_replay_impl.cuh — the device trace-replay engine (R5-R21): whole
-// discrete-event replays of the Strait scheduler, ONE WARP PER REPLAY, the
-// replay's entire mutable state resident in that warp's slice of shared
-// memory.  Instantiated once per metric count in strait_replay_nm*.cu.
+// discrete-event replays of the Strait scheduler, the replay's entire mutable
+// state resident in shared memory.  One warp per replay (replay sweeps, narrow
+// nodes), or one CTA of 8 warps per replay for wide nodes: a master warp runs
+// the event loop and the helper warps join its wide steps (Sim<..., NW>).
+// Instantiated once per metric count in strait_replay_nm*.cu.
 //
 // Restates /root/reference/pkg/src/infersim/simulation.py:122-513 driving
 // PredictivePolicy (scheduler.py:229-378), InterferencePredictor
