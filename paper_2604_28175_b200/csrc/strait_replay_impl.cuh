@@ -982,23 +982,26 @@ struct Sim : Geom<GEOM> {
       bool hp = false, hm = false;
       int s = 0, ep = 0, pgi = 0, ci = 0, g2 = 0;
       double xp = 1.0, xm = 1.0;
-      if (i < ni) {  // A1: check_violate's projection of running entry ci of GPU g (scheduler.py:137-160)
+      if (i < ni) {  // A1: check_violate's projection of the entry in slot ci of GPU g (scheduler.py:137-160)
+        // items walk a GPU's slots, not its list positions: check_violate's
+        // boolean is an OR over the running entries, so the order is immaterial,
+        // and the slot's fields load without first reading the running list
         pgi = i / CONC, ci = i - pgi * CONC;
         const int kq = pgi / NG, g = pgi - kq * NG;
+        s = slot(g, ci);
         const int n = GI(GI_NRUN, g);
+        const bool live = SB(SB_LIVE, s);
+        ep = SB(SB_PRIO, s);
         if (n < CONC) {  // else has_slot fails: phase B never reads this pair's items
-          if (ci < n) {
-            s = slot_at(g, ci);
-            ep = SB(SB_PRIO, s);
-            if (ep <= cprio) {
-              Cand cd;
+          if (live && ep <= cprio) {
+            Cand cd;
 #pragma unroll
-              for (int q = 0; q < NM; ++q) cd.c[q] = thr(m, k0 + kq + 1, q);
-              xp = proj_x(s, cd);
-              hp = true;
-            }
+            for (int q = 0; q < NM; ++q) cd.c[q] = thr(m, k0 + kq + 1, q);
+            xp = proj_x(s, cd);
+            hp = true;
+          } else {
+            pv[pgi * C1 + ci] = 0;
           }
-          if (!hp) pv[pgi * C1 + ci] = 0;
         }
       }
       Cand cm;
