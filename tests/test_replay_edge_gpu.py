@@ -2,7 +2,8 @@
 oracle (itself pinned to the reference by tests/test_replay_oracle.py):
 an empty replay, more models than warp lanes (40), more GPUs than lanes (48,
 the probe-by-probe propose path) with several concurrency limits and batch
-sizes up to 16, every policy in one mixed launch, and device-generated inputs."""
+sizes up to 16, every policy in one mixed launch, device-generated inputs, and a
+wide node with batch sizes up to 40 and the baseline policies."""
 import numpy as np
 import pytest
 
@@ -124,3 +125,18 @@ def test_fixed_geometry_kernel_rejects_a_wrong_uniform_flag(cuda):
     assert int(res.counters[0, 0]) == 0 and int(res.counters[1, 0]) != 0
     with pytest.raises(ValueError):
         res.check()
+
+
+def test_wide_node_large_batches_and_baselines(cuda, oracle):
+    """A 16-GPU node (64 slots: the CTA-per-replay layout) with batch sizes up
+    to 40 (beyond the 32 sizes the CTA propose job covers, so the master warp's
+    probe-by-probe search runs inside the CTA kernel), and every baseline
+    policy on the same wide node."""
+    from paper_2604_28175_b200.replay import ReplaySpec
+
+    profs = _profiles(8, seed=5, max_batch=40)
+    rates = {m: 1500.0 for m in profs}
+    specs = [ReplaySpec(_cfg(profs, rates, 120.0, 16, 4, seed=4), 4)]
+    specs += [ReplaySpec(_cfg(profs, rates, 120.0, 16, 4, policy=p, seed=5 + i), 5 + i)
+              for i, p in enumerate(("temporal", "static", "reactive"))]
+    _check(specs, oracle)
