@@ -102,6 +102,11 @@ constexpr int kKC = 0, kTC = 1, kARR = 2, kTO = 3, kTICK = 4;  // simulation.py:
 constexpr double kWorkEps = 1e-9;                               // simulation.py:35
 constexpr unsigned long long kNoKey = ~0ULL;
 constexpr int kMaxConc = 32;  // lane-per-list-position steps (recompute, restamp, intf_cur of a GPU)
+// event homes above which the CTA layout scans them as a job (STRAIT_SELECT_JOB_MIN at build time)
+#ifndef STRAIT_SELECT_JOB_MIN
+#define STRAIT_SELECT_JOB_MIN 1024
+#endif
+constexpr int kSelectJobMin = STRAIT_SELECT_JOB_MIN;
 constexpr int kMaxModels = 64;
 constexpr int kMaxBatch = 64;
 constexpr unsigned kFull = 0xffffffffu;
@@ -1678,7 +1683,7 @@ struct Sim : Geom<GEOM> {
   // ------------------------------------------------------------ next event
   // this thread's share of the event homes: i = first, first + step, ...
   __device__ __forceinline__ void scan_homes(int first, int step, double& bt, unsigned long long& bk, int& bi) const {
-#pragma unroll 1
+#pragma unroll 4
     for (int i = first; i < NE; i += step) {
       const double t = ed[i];
       const unsigned long long kk = ek[i];
@@ -1805,7 +1810,7 @@ struct Sim : Geom<GEOM> {
       unsigned long long bk = kNoKey;
       int bi = -1;
       bool wide = false;
-      if constexpr (CTA) wide = NE > 32;
+      if constexpr (CTA) wide = NE > kSelectJobMin;
       if (wide) {  // JOB_SELECT: every warp scans a share of the homes; lane w takes warp w's minimum
         if (lane == 0) jb->kind = JOB_SELECT;
         post_job();
