@@ -102,11 +102,6 @@ constexpr int kKC = 0, kTC = 1, kARR = 2, kTO = 3, kTICK = 4;  // simulation.py:
 constexpr double kWorkEps = 1e-9;                               // simulation.py:35
 constexpr unsigned long long kNoKey = ~0ULL;
 constexpr int kMaxConc = 32;  // lane-per-list-position steps (recompute, restamp, intf_cur of a GPU)
-// event homes above which the CTA layout scans them as a job (STRAIT_SELECT_JOB_MIN at build time)
-#ifndef STRAIT_SELECT_JOB_MIN
-#define STRAIT_SELECT_JOB_MIN 1024
-#endif
-constexpr int kSelectJobMin = STRAIT_SELECT_JOB_MIN;
 constexpr int kMaxModels = 64;
 constexpr int kMaxBatch = 64;
 constexpr unsigned kFull = 0xffffffffu;
@@ -132,17 +127,16 @@ enum { QI_HEAD, QI_TAIL, QI_FGEN, QI_TGEN, QI_EGEN, QI_ORD, QI_N };
 
 // Job block of a CTA-per-replay launch (NW > 1 warps per replay, below): the
 // master warp posts one of these, the helper warps read it after barrier 1.
-enum { JOB_EXIT, JOB_ICUR, JOB_PROPOSE, JOB_SELECT };
+enum { JOB_EXIT, JOB_ICUR, JOB_PROPOSE };
 struct Job {
   int kind, m, kmax, cprio, k0, pad;
   double now, dl, front;
   long long t0;  // profiling build: the master's clock at the post
 };
-// one warp's partial of a reduction: an event-home minimum, or a size's best GPU
+// one warp's partial of a reduction: a size's best GPU over a chunk of 32 GPUs
 struct Part {
-  double t, x;
-  unsigned long long key;
-  int g, pad;
+  double t, x;  // latency, interference of the chunk's best GPU
+  int g, pad;   // its gpu_id, -1 if none feasible
 };
 
 struct Layout {
@@ -188,7 +182,7 @@ struct Layout {
       pintf = take(8 * kg);
       pm = take(kg);
       const size_t np = (size_t)cta_sizes(b) * cta_chunks(G);
-      part = take(sizeof(Part) * (np > (size_t)nw ? np : (size_t)nw));
+      part = take(sizeof(Part) * np);
     }
     bytes = o;
   }
@@ -243,8 +237,8 @@ struct Geom<3> {
 // NW = warps per replay.  NW = 1: one warp runs the whole replay.  NW > 1 (one
 // replay per CTA, for single replays and few-replay launches): warp 0 (the
 // master) runs the event loop exactly as with NW = 1; at the wide steps —
-// intf_cur of every running entry, a propose's (size, GPU, co-runner)
-// projections, and the next-event scan over many homes — it posts a Job and
+// intf_cur of every running entry and a propose's (size, GPU, co-runner)
+// projections and meets — it posts a Job and
 // the NW - 1 helper warps, parked on named barrier 1, join it.  Every job reads
 // the replay state and writes only per-item scratch (or per-slot caches that
 // no other item touches); barrier 2 ends it.  Same arithmetic, same bits.
@@ -1082,7 +1076,7 @@ struct Sim : Geom<GEOM> {
           bi = i2;
         }
       }
-      if ((lane & (seg - 1)) == 0 && kq < kmax) part[kq * nch + (g >> 5)] = Part{bl, bi, 0ull, found ? bg : -1, 0};
+      if ((lane & (seg - 1)) == 0 && kq < kmax) part[kq * nch + (g >> 5)] = Part{bl, bi, found ? bg : -1, 0};
     }
     if (w == 0) RP_ADD(RPF_CTA_PB, t_pb);  // the master's phase-B pairs
 #if STRAIT_REPLAY_PROFILE
@@ -1708,17 +1702,6 @@ struct Sim : Geom<GEOM> {
     bt = __longlong_as_double((long long)(((unsigned long long)m0 << 32) | m1));
     bi = __shfl_sync(kFull, bi, __ffs(__ballot_sync(kFull, c)) - 1);
   }
-  // JOB_SELECT (every warp of the CTA): warp w's minimum into part[w]
-  __device__ __forceinline__ void job_select() const {
-    double bt = __longlong_as_double(0x7ff0000000000000LL);
-    unsigned long long bk = kNoKey;
-    int bi = -1;
-    scan_homes(w * 32 + lane, NT, bt, bk, bi);
-    warp_min_event(bt, bk, bi);
-    if (lane == 0) part[w] = Part{bt, 0.0, bk, bi, 0};
-    cta_bar(2);
-  }
-
   // helper warps (NW > 1): parked on barrier 1 until the master posts a job
   __device__ void helper_loop() {
     for (;;) {
@@ -1726,10 +1709,6 @@ struct Sim : Geom<GEOM> {
       const int kind = jb->kind;
       if (kind == JOB_EXIT) return;
       const double now = jb->now;
-      if (kind == JOB_SELECT) {
-        job_select();
-        continue;
-      }
       load_shared_pred();
       if (kind == JOB_ICUR) job_icur(now);
       else job_propose(jb->m, jb->k0, jb->kmax, jb->cprio, jb->dl, jb->front, now);
@@ -1809,21 +1788,9 @@ struct Sim : Geom<GEOM> {
       double bt = INF;
       unsigned long long bk = kNoKey;
       int bi = -1;
-      bool wide = false;
-      if constexpr (CTA) wide = NE > kSelectJobMin;
-      if (wide) {  // JOB_SELECT: every warp scans a share of the homes; lane w takes warp w's minimum
-        if (lane == 0) jb->kind = JOB_SELECT;
-        post_job();
-        job_select();
-        if (lane < NW) {
-          const Part q = part[lane];
-          bt = q.t;
-          bk = q.key;
-          bi = q.g;
-        }
-      } else {
-        scan_homes(lane, 32, bt, bk, bi);
-      }
+      // (the CTA layout scans on the master too: with the scan unrolled, a scan
+      // job's wake-up costs what splitting the homes saves)
+      scan_homes(lane, 32, bt, bk, bi);
       warp_min_event(bt, bk, bi);
       if (bk == kNoKey) break;
       sync();  // the scan's reads of the event homes complete before any handler writes them

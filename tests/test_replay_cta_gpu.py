@@ -1,7 +1,7 @@
 """GPU parity of both replay-engine layouts on every reference golden replay:
 one warp per replay (STRAIT_REPLAY_NW=1) and one CTA of 8 warps per replay
 (STRAIT_REPLAY_NW=8: the master warp runs the event loop, the helper warps
-join the intf_cur, propose and next-event jobs).  The launcher picks the CTA
+join the intf_cur and propose jobs).  The launcher picks the CTA
 layout by itself only for wide geometries (more running-batch slots than a
 warp has lanes, e.g. C5's 64 GPUs); forcing it here runs the CTA jobs on
 every geometry, including the all-sizes propose job (few GPUs) and the
