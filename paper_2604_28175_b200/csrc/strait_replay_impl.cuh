@@ -860,21 +860,22 @@ struct Sim : Geom<GEOM> {
   };
 
   // lexicographic (latency, gpu_id) argmin across the warp (best_for's tie-break)
+  // as three 32-bit warp reductions on an order-preserving image of the latency
+  // (-0 folded onto +0, so equal latencies tie on gpu_id as in the scan), then
+  // the winner's fields
   __device__ __forceinline__ Plan warp_best(bool found, int bg, double bl, double bi) const {
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      const bool f2 = __shfl_xor_sync(kFull, found, off);
-      const int g2 = __shfl_xor_sync(kFull, bg, off);
-      const double l2 = __shfl_xor_sync(kFull, bl, off);
-      const double i2 = __shfl_xor_sync(kFull, bi, off);
-      if (f2 && (!found || l2 < bl || (l2 == bl && g2 < bg))) {
-        found = true;
-        bg = g2;
-        bl = l2;
-        bi = i2;
-      }
-    }
-    return Plan{found, bg, bl, bi};
+    unsigned long long lb = (unsigned long long)__double_as_longlong(bl == 0.0 ? 0.0 : bl);
+    lb = (lb >> 63) ? ~lb : lb | 0x8000000000000000ull;
+    const unsigned h = found ? (unsigned)(lb >> 32) : ~0u, lo = found ? (unsigned)lb : ~0u;
+    const unsigned m0 = __reduce_min_sync(kFull, h);
+    bool c = found && h == m0;
+    const unsigned m1 = __reduce_min_sync(kFull, c ? lo : ~0u);
+    c = c && lo == m1;
+    const unsigned m2 = __reduce_min_sync(kFull, c ? (unsigned)bg : ~0u);
+    c = c && (unsigned)bg == m2;
+    const unsigned who = __ballot_sync(kFull, c);
+    const int src = who ? __ffs(who) - 1 : 0;
+    return Plan{who != 0, __shfl_sync(kFull, bg, src), __shfl_sync(kFull, bl, src), __shfl_sync(kFull, bi, src)};
   }
 
   // best_for(k) with lanes over GPUs
@@ -1064,27 +1065,9 @@ struct Sim : Geom<GEOM> {
         bl = plat[pg];
         bi = pintf[pg];
       }
-      if (seg == 32) {
-        // a whole warp is one size's chunk of 32 GPUs: the lexicographic
-        // (latency, gpu_id) minimum as three 32-bit warp reductions on an
-        // order-preserving image of the latency (-0 folded onto +0, so equal
-        // latencies tie on gpu_id as in the scan), then the winner's fields
-        const double l0 = bl == 0.0 ? 0.0 : bl;
-        unsigned long long lb = (unsigned long long)__double_as_longlong(l0);
-        lb = (lb >> 63) ? ~lb : lb | 0x8000000000000000ull;
-        const unsigned h = found ? (unsigned)(lb >> 32) : ~0u, lo = found ? (unsigned)lb : ~0u;
-        const unsigned m0 = __reduce_min_sync(kFull, h);
-        bool c = found && h == m0;
-        const unsigned m1 = __reduce_min_sync(kFull, c ? lo : ~0u);
-        c = c && lo == m1;
-        const unsigned m2 = __reduce_min_sync(kFull, c ? (unsigned)bg : ~0u);
-        c = c && (unsigned)bg == m2;
-        const unsigned who = __ballot_sync(kFull, c);
-        const int src = who ? __ffs(who) - 1 : 0;
-        found = who != 0;
-        bg = __shfl_sync(kFull, bg, src);
-        bl = __shfl_sync(kFull, bl, src);
-        bi = __shfl_sync(kFull, bi, src);
+      if (seg == 32) {  // a whole warp is one size's chunk of 32 GPUs
+        const Plan b = warp_best(found, bg, bl, bi);
+        found = b.ok, bg = b.gpu, bl = b.lat, bi = b.intf;
       } else {
         for (int off = seg >> 1; off; off >>= 1) {
           const bool f2 = __shfl_xor_sync(kFull, found, off);
