@@ -1211,33 +1211,22 @@ struct Sim : Geom<GEOM> {
         load_cand(m, k, cd);
         found = eval_pair(g, cd, cprio, dl, front, now, bl, bi);
       }
-      // segmented lexicographic (latency, gpu_id) argmin within each size's W lanes
-      for (int off = W >> 1; off; off >>= 1) {
-        const bool f2 = __shfl_xor_sync(kFull, found, off);
-        const int g2 = __shfl_xor_sync(kFull, bg, off);
-        const double l2 = __shfl_xor_sync(kFull, bl, off);
-        const double i2 = __shfl_xor_sync(kFull, bi, off);
-        if (f2 && (!found || l2 < bl || (l2 == bl && g2 < bg))) {
-          found = true;
-          bg = g2;
-          bl = l2;
-          bi = i2;
-        }
-      }
-      const unsigned feas = __ballot_sync(kFull, found && g == 0);  // bit (k-1)*W: best_for(k) is not None
+      // best_for(k) is not None iff some lane of size k's W-lane segment found a
+      // pair: the binary search's probes run on those bits, and only the chosen
+      // size's (latency, gpu_id) argmin is reduced (warp reductions over the
+      // segment's lanes)
+      const unsigned fb = __ballot_sync(kFull, found);
+      const unsigned segmask = W == 32 ? ~0u : (1u << W) - 1;
       while (lo <= hi) {
         const int mid = (lo + hi) / 2;
-        if (feas >> ((mid - 1) << lw) & 1u) {
+        if (fb >> ((mid - 1) << lw) & segmask) {
           bestk = mid;
           lo = mid + 1;
         } else {
           hi = mid - 1;
         }
       }
-      if (bestk) {
-        const int src = (bestk - 1) << lw;
-        plan = Plan{true, __shfl_sync(kFull, bg, src), __shfl_sync(kFull, bl, src), __shfl_sync(kFull, bi, src)};
-      }
+      if (bestk) plan = warp_best(found && k == bestk, bg, bl, bi);
       return bestk;
     }
     if constexpr (LEAN) {  // the launcher chose LEAN for a geometry that cannot reach here
