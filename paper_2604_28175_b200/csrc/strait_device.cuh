@@ -108,6 +108,17 @@ struct Pred {
     bool s;
     return predict(a, cmp, mem, prio, s);
   }
+  // exp(z1), exp(z2) as one block (interleaved chains); bit-identical to two exp calls
+  __device__ __forceinline__ void exp2v(double z1, double z2, double& e1, double& e2) const {
+#if STRAIT_LIBM
+    bool special = false;
+    e1 = glibc::exp_common(z1, etab, special);
+    e2 = glibc::exp_common(z2, etab, special);
+    if (!special) return;
+#endif
+    e1 = MathT::exp(z1, etab);
+    e2 = MathT::exp(z2, etab);
+  }
   // Two kernel_effect()s as one block, so their exp chains interleave when exp
   // is inlined (bit-identical to two effect() calls; the inputs that need the
   // saturation or exp()'s special cases take effect() itself).

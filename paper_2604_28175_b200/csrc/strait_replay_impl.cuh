@@ -291,6 +291,8 @@ struct Sim : Geom<GEOM> {
   int lp_allowance;   // ReactiveState (baselines.py:81-110)
   double last_reset;
   int64_t next_arr, resolved;
+  double my_dl, my_floor, my_to;  // lane m < 32: model m's deadline, total(1), batch timeout
+  int my_maxb;                    // and max batch size
   int64_t pf_q, pf_g;  // the last arrival's queue-order check, settled at the next arrival / the end
   int pf_m;            // model of the next arrival
   double pf_t2;        // time of the arrival after the next
@@ -632,12 +634,16 @@ struct Sim : Geom<GEOM> {
     const double cap = pr.cap;
     const double x = pr.exponent(tw, cmp, mem);
     const double z = x * pr.log_base;
-    double inner, pow_bx = 0.0;
+    double inner, pow_bx = 0.0, pow_bx1 = 0.0;  // b^x, and b^(x-1) for lane 1's gradient term
     if (z > kLogSaturate) {
       saturated = true;
       inner = __longlong_as_double(0x7ff0000000000000LL);
     } else {
-      pow_bx = MathT::exp(z, pr.etab);
+      if constexpr (MathT::kInline) {  // both exps as one block, on every lane (no divergent exp)
+        pr.exp2v(z, (x - 1.0) * pr.log_base, pow_bx, pow_bx1);
+      } else {
+        pow_bx = MathT::exp(z, pr.etab);
+      }
       inner = pr.scale * pow_bx + pr.offset;
       saturated = inner >= cap;
     }
@@ -651,7 +657,7 @@ struct Sim : Geom<GEOM> {
       const double log_b = pr.log_base;
       const double zz = pr.scale * pow_bx;
       if (lane == 0) d = pow_bx * cfc;
-      else if (lane == 1) d = pr.scale * x * MathT::exp((x - 1.0) * log_b, pr.etab) * cfc;
+      else if (lane == 1) d = pr.scale * x * (MathT::kInline ? pow_bx1 : MathT::exp((x - 1.0) * log_b, pr.etab)) * cfc;
       else if (lane == 2) d = cfc;
       else if (lane < 3 + NM) {
         double ai = 0.0;
@@ -1420,8 +1426,12 @@ struct Sim : Geom<GEOM> {
         const int len = q_len(m);
         if (len) {
           const double fr = front_arrival(m);
-          d = (fr + mdeadline(m)) - now < tab_total(m, 1);  // early_drop's front test (scheduler.py:65-75)
-          e = len >= mmaxb(m) || now >= fr + mtimeout(m);
+          // lane m's model constants stay in registers (M <= 32, loaded once in run())
+          const double mdl = m0 == 0 ? my_dl : mdeadline(m), mfl = m0 == 0 ? my_floor : tab_total(m, 1);
+          const double mto = m0 == 0 ? my_to : mtimeout(m);
+          const int mmb = m0 == 0 ? my_maxb : mmaxb(m);
+          d = (fr + mdl) - now < mfl;  // early_drop's front test (scheduler.py:65-75)
+          e = len >= mmb || now >= fr + mto;
         }
       }
       dropm |= (unsigned long long)__ballot_sync(kFull, d) << m0;
@@ -1762,6 +1772,10 @@ struct Sim : Geom<GEOM> {
     c_cap_rows = NG;
     seq = (unsigned long long)N;  // the arrivals took seq 1..N (simulation.py:184-194)
     next_arr = 0;
+    my_dl = lane < M ? mdeadline(lane) : 0.0;
+    my_floor = lane < M ? tab_total(lane, 1) : 0.0;
+    my_to = lane < M ? mtimeout(lane) : 0.0;
+    my_maxb = lane < M ? mmaxb(lane) : 0;
     pf_q = pf_g = 0;
     pf_m = N ? (int)__ldg(&A->arr_model[base]) : 0;
     pf_t2 = N > 1 ? arr(base + 1) : INF;
