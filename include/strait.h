@@ -68,7 +68,9 @@ int strait_last_sweep_path(void);
  * 1 log(x), 2 pow(x, y), 3 log1p(x) — restatements of glibc 2.39's
  * exp/log/pow/log1p (the libm behind CPython's math.exp, math.log and
  * float.__pow__, which predictor.py:136-137,181-184,289-293 and oracle.py:73
- * call, and behind numpy's ziggurat tails).  y may be NULL unless fn == 2.
+ * call, and behind numpy's ziggurat tails).  fn 4 is x / y through the
+ * engine's certified shared-divisor division (must equal IEEE division).
+ * y may be NULL unless fn == 2 or 4.
  */
 int strait_math(int32_t fn, const double *x, const double *y, int64_t n, double *out, void *stream);
 

@@ -41,6 +41,44 @@ constexpr int kMaxP = STRAIT_MAX_METRICS + 7;
 __host__ __device__ __forceinline__ double py_max(double a, double b) { return (b > a) ? b : a; }
 __host__ __device__ __forceinline__ double py_min(double a, double b) { return (b < a) ? b : a; }
 
+// q[i] = a[i] / b for i < N, each the correctly rounded binary64 quotient (as
+// __ddiv_rn), with ONE divisor: the reciprocal is formed once (rcp.approx +
+// two Newton steps), each quotient gets one Markstein step, and each is then
+// CERTIFIED exactly — the residual r = a - q*b is exact (FMA, operands in
+// range), and |r| < ulp(q)/2 * |b| with q not a power of two proves q is the
+// nearest binary64 to a/b.  Any operand out of range, any tie or any failed
+// certificate sends all N to __ddiv_rn.  Straight-line in the common case, so
+// the N quotients overlap (N sequential __ddiv_rn do not: each carries its
+// slow-path branch).
+template <int N>
+__device__ __forceinline__ void div_shared(const double (&a)[N], double b, double (&q)[N]) {
+  const double ab = fabs(b);
+  bool ok = ab >= 0x1p-400 && ab <= 0x1p400;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
+  double e = __fma_rn(-b, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-b, r, 1.0);
+  r = __fma_rn(r, e, r);
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const double q0 = a[i] * r;
+    const double q1 = __fma_rn(__fma_rn(-b, q0, a[i]), r, q0);
+    const double res = __fma_rn(-b, q1, a[i]);  // a - q1*b, exact
+    const unsigned long long qb = (unsigned long long)__double_as_longlong(q1);
+    const int ex = (int)((qb >> 52) & 0x7ff);
+    // |q1| in [2^-400, 2^400] and not a power of two (its lower neighbour is a full ulp away)
+    ok = ok && ex >= 1023 - 400 && ex <= 1023 + 400 && (qb & 0xfffffffffffffull) != 0;
+    const double half_ulp = __longlong_as_double((long long)((unsigned long long)(ex - 53) << 52));
+    ok = ok && fabs(res) < half_ulp * ab;
+    q[i] = q1;
+  }
+  if (!ok) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) q[i] = __ddiv_rn(a[i], b);
+  }
+}
+
 // Transcendental policy of the predictor: inlined (default), or routed by a
 // kernel to shared out-of-line copies (MathT with the same static members).
 struct InlineMath {

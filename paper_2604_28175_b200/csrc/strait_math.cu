@@ -12,6 +12,12 @@ __global__ void math_kernel(int fn, const double* __restrict__ x, const double* 
                             double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double a = x[i];
+    if (fn == 4) {  // the certified shared-divisor quotient (strait_device.cuh div_shared), one element
+      double num[1] = {a}, q[1];
+      strait::div_shared(num, y[i], q);
+      out[i] = q[0];
+      continue;
+    }
     out[i] = fn == 0 ? strait::dexp(a) : fn == 1 ? strait::dlog(a) : fn == 2 ? strait::dpow(a, y[i])
                                                                   : strait::glibc::log1p(a);
   }
@@ -46,7 +52,7 @@ extern "C" int strait_gt_slowdown(const StraitGroundTruth* gt, const double* co,
 }
 
 extern "C" int strait_math(int32_t fn, const double* x, const double* y, int64_t n, double* out, void* stream) {
-  if (fn < 0 || fn > 3 || n < 0 || (n && (!x || !out || (fn == 2 && !y))))
+  if (fn < 0 || fn > 4 || n < 0 || (n && (!x || !out || ((fn == 2 || fn == 4) && !y))))
     return strait::set_error(STRAIT_EINVAL, "strait_math: bad arguments");
   if (!n) return STRAIT_OK;
   const int64_t blocks64 = (n + 255) / 256;

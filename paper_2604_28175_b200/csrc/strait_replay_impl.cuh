@@ -473,8 +473,15 @@ struct Sim : Geom<GEOM> {
       return;
     }
     const double d = end - SD(SD_TL, s);
+    if constexpr (MathT::kInline) {  // the NM quotients by one total overlap (div_shared)
+      double num[NM];
 #pragma unroll
-    for (int i = 0; i < NM; ++i) out[i] = MathT::div(SD(SD_ACC + i, s) + SD(SD_VL + i, s) * d, total);
+      for (int i = 0; i < NM; ++i) num[i] = SD(SD_ACC + i, s) + SD(SD_VL + i, s) * d;
+      div_shared(num, total, out);
+    } else {
+#pragma unroll
+      for (int i = 0; i < NM; ++i) out[i] = MathT::div(SD(SD_ACC + i, s) + SD(SD_VL + i, s) * d, total);
+    }
   }
 
   // ------------------------------------------------------------ runtime (runtime.py:104-141)

@@ -83,3 +83,29 @@ def test_log1p_bit_exact(cuda):
                         np.exp(rng.uniform(-40, 40, 20_000)), [0.0, -0.0, -0.5, -0.2929, 0.41422, 1e-300,
                                                                 -1e-20, 3e-9, 2.0 ** 53, 1e300]])
     _check(3, math.log1p, x)
+
+
+def test_certified_division_equals_ieee(cuda):
+    """The replay engine's shared-divisor division (div_shared: one reciprocal,
+    a Markstein step, an exact residual certificate, __ddiv_rn otherwise)
+    equals IEEE binary64 division bit for bit: random operands over wide and
+    TWA-like ranges, quotients at powers of two and at ties, and the special
+    values that take the fallback."""
+    rng = np.random.default_rng(11)
+    n = 1_000_000
+    a = np.concatenate([rng.uniform(0, 50, n), np.exp(rng.uniform(-700, 700, n // 4)) * rng.choice([-1, 1], n // 4),
+                        rng.integers(1, 1 << 53, n // 4).astype(np.float64)])
+    b = np.concatenate([rng.uniform(1e-3, 30, n), np.exp(rng.uniform(-700, 700, n // 4)),
+                        rng.integers(1, 1 << 20, n // 4).astype(np.float64)])
+    # exact quotients (powers of two, small integers) and halfway-adjacent cases
+    k = rng.integers(1, 1 << 20, 50_000).astype(np.float64)
+    a = np.concatenate([a, k * 8.0, k * 3.0, k + 0.5, [1.0, 0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 1e308, 3.0]])
+    b = np.concatenate([b, k, np.full(50_000, 3.0), np.full(50_000, 2.0),
+                        [3.0, 7.0, 7.0, 2.0, 2.0, 2.0, 3.0, 1e-308, 0.0]])
+    got = device_math(4, a, b)
+    with np.errstate(all="ignore"):
+        want = a / b
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(got), nan)
+    diff = np.flatnonzero(bits(got)[~nan] != bits(want)[~nan])
+    assert diff.size == 0, f"{diff.size} differ; e.g. {a[~nan][diff[:3]]} / {b[~nan][diff[:3]]}"
