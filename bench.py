@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true", help="skip the oracle parity checks (timing only)")
     ap.add_argument("--replay-steps", type=int, default=3, help="timed launches of the C4 replay sweep")
+    ap.add_argument("--replay-e2e-steps", type=int, default=8, help="pipelined end-to-end steps of the C4 sweep")
     ap.add_argument("--replay-seeds", type=int, default=16, help="seeds per C4 grid point (16 = BASELINE C4)")
     ap.add_argument("--no-replay", action="store_true", help="C3 only")
     ap.add_argument("--no-single", action="store_true", help="skip the single-replay legs (C1, C2, C5)")
@@ -528,26 +529,31 @@ def c4_leg(args, ws, rank, dist):
     # descriptions H2D, device stream generation) is built on a second stream while step i runs,
     # and step i's result() copies outcomes + counters + metrics back.
     fetch = {"counters", "req_status", "req_violated"}
-    s_build, s_run = torch.cuda.Stream(), torch.cuda.Stream()
+    s_build, s_run, s_copy = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
 
     def build():
         with torch.cuda.stream(s_build):
             return ReplayBatch(specs, generate="device")
 
     def e2e_pipeline(n):
+        # step i runs on s_run while step i+1 is built on s_build and step i-1's
+        # outputs come back on s_copy (result() ordered after its own launch only)
         t0 = time.perf_counter()
-        nxt, res = build(), None
+        nxt, prev, res = build(), None, None
         for i in range(n):
             cur = nxt
             s_run.wait_stream(s_build)
             pend = cur.launch(stream=s_run, metrics=True)
             nxt = build() if i + 1 < n else None
-            res = pend.result(fetch=fetch)
+            if prev is not None:
+                res = prev.result(fetch=fetch, copy_stream=s_copy)
+            prev = pend
+        res = prev.result(fetch=fetch, copy_stream=s_copy)
         torch.cuda.synchronize()
         return (time.perf_counter() - t0) * 1e3 / n, res
 
     e2e_pipeline(1)
-    e2e_ms, res2 = e2e_pipeline(4)
+    e2e_ms, res2 = e2e_pipeline(args.replay_e2e_steps)
     b2 = res2.batch
     h2d = int(sum(np.asarray(v).nbytes for k, v in b2.inputs.items() if k != "cfg") + len(bytes(b2.inputs["cfg"])))
     d2h = int(sum(v.nbytes for k, v in res2.a.items() if k in fetch or k.startswith("m_")))
@@ -576,7 +582,8 @@ def c4_leg(args, ws, rank, dist):
                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                    "path": "ReplayBatch(specs, generate='device').launch() / .result(): configs + stream specs "
                            "H2D -> device streams -> strait_replay -> device metrics -> D2H outcomes (wall clock); "
-                           "4 steps pipelined (step i+1's batch built on a second stream while step i runs)"},
+                           f"{args.replay_e2e_steps} steps pipelined (step i+1's batch built and step i-1's "
+                           "outputs copied back on other streams while step i runs)"},
            "host_input_build_s": build_s, "gpu_launches": launches, "assignment": {"policy": "LPT", "ranks": per_rank},
            "bound": "latency (one warp per replay); no roofline claim, DESIGN.md 3.3"}
     if par is not None:

@@ -374,7 +374,9 @@ class ReplayBatch:
             raise ValueError("launch() is for untraced batches; use run() with trace=True")
         with _on(stream):
             din, dout, mout = self._enqueue(metrics)
-        return PendingReplay(self, din, dout, mout, stream, metrics)
+            done = torch.cuda.Event()
+            done.record()
+        return PendingReplay(self, din, dout, mout, stream, metrics, done)
 
     def run(self, stream=None, metrics: bool = True, fetch=None) -> "ReplayResult":
         """Host in, device replay (+ device metrics), host out, every step on
@@ -408,12 +410,18 @@ def _collect(din, dout, mout, fetch) -> dict:
 class PendingReplay:
     """A launched replay batch (ReplayBatch.launch); result() copies it back."""
 
-    def __init__(self, batch, din, dout, mout, stream, metrics=True):
+    def __init__(self, batch, din, dout, mout, stream, metrics=True, done=None):
         self.batch, self.din, self.dout, self.mout, self.stream = batch, din, dout, mout, stream
-        self.metrics = metrics
+        self.metrics, self.done = metrics, done
 
-    def result(self, fetch=None) -> "ReplayResult":
-        with _on(self.stream):
+    def result(self, fetch=None, copy_stream=None) -> "ReplayResult":
+        """Wait for this replay and copy it back.  With `copy_stream` the copies
+        run there, ordered after this launch only, so a batch launched since on
+        the launch stream keeps running while they proceed."""
+        on = copy_stream if copy_stream is not None else self.stream
+        with _on(on):
+            if copy_stream is not None and self.done is not None:
+                copy_stream.wait_event(self.done)
             if self.batch._overflow(D.host(self.dout["counters"])):  # cap rows overflowed: exact re-run
                 return self.batch.run(self.stream, self.metrics, fetch)
             return ReplayResult(self.batch, _collect(self.din, self.dout, self.mout, fetch))
