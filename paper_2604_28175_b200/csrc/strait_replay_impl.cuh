@@ -101,6 +101,9 @@ struct FullInlineMath : InlineMath {
 constexpr int kKC = 0, kTC = 1, kARR = 2, kTO = 3, kTICK = 4;  // simulation.py:28-33 tie ranks
 constexpr double kWorkEps = 1e-9;                               // simulation.py:35
 constexpr unsigned long long kNoKey = ~0ULL;
+#ifndef STRAIT_CTA_PROBE_ITEMS
+#define STRAIT_CTA_PROBE_ITEMS 2  // CTA propose: probe-by-probe jobs above this many items per thread
+#endif
 constexpr int kMaxConc = 32;  // lane-per-list-position steps (recompute, restamp, intf_cur of a GPU)
 constexpr int kMaxModels = 64;
 constexpr int kMaxBatch = 64;
@@ -1144,7 +1147,7 @@ struct Sim : Geom<GEOM> {
     const double dl = mdeadline(m);
     const int nch = Layout::cta_chunks(NG);
     int lo = 1, hi = kmax, bestk = 0;
-    if (kmax * NG * (CONC + 1) > 2 * NT) {
+    if (kmax * NG * (CONC + 1) > STRAIT_CTA_PROBE_ITEMS * NT) {
       while (lo <= hi) {
         const int mid = (lo + hi) / 2;
         run_propose_job(m, mid - 1, 1, cprio, dl, front, now);
