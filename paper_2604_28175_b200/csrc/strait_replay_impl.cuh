@@ -248,7 +248,10 @@ struct Geom<3> {
 // ILP: eval_pair evaluates check_meet and the co-runner projections two exp
 // chains at a time (Pred::effect2) — the lower latency for single replays; a
 // launch with several replays per SM keeps the smaller one-chain code, which
-// the instruction cache rewards there.
+// the instruction cache rewards there, and so do the generic CTA-layout
+// kernels, whose proposes run as jobs (eval_pair only for batches past 32
+// sizes) and whose 256 threads leave at most 255 registers (the C5-geometry
+// CTA kernel measured faster with it, spills included).
 template <int NM, typename MathT, bool TR, bool LEAN, int GEOM, int NW = 1, bool ILP = true>
 struct Sim : Geom<GEOM> {
   using Geom<GEOM>::G;
@@ -2045,15 +2048,15 @@ int launch_replay_occ(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_
   int launch_replay<NMV>(const StraitReplayArgs& a, cudaStream_t st, int wpc, size_t smem_per_warp, int minb) { \
     const bool po = lean_batch(a);                                                                                \
     if (minb == 3) /* traced, geometry past the one-warp budget: CTA per replay with the event log */           \
-      return launch_replay_occ<NMV, 1, true, false, 0, kCtaWarps>(a, st, wpc, smem_per_warp);                    \
+      return launch_replay_occ<NMV, 1, true, false, 0, kCtaWarps, false>(a, st, wpc, smem_per_warp);                    \
     if (minb == 2) { /* CTA per replay: single replays and few-replay launches */                                \
       if constexpr (NMV == 5) {                                                                                   \
         if (c5_geometry(a)) return launch_replay_occ<NMV, 1, false, false, 3, kCtaWarps>(a, st, wpc, smem_per_warp); \
         if (po && overload_geometry(a) && a.models.stride == 8)                                                   \
-          return launch_replay_occ<NMV, 1, false, true, 2, kCtaWarps>(a, st, wpc, smem_per_warp);                \
+          return launch_replay_occ<NMV, 1, false, true, 2, kCtaWarps, false>(a, st, wpc, smem_per_warp);                \
       }                                                                                                           \
-      return po ? launch_replay_occ<NMV, 1, false, true, 0, kCtaWarps>(a, st, wpc, smem_per_warp)                \
-                : launch_replay_occ<NMV, 1, false, false, 0, kCtaWarps>(a, st, wpc, smem_per_warp);              \
+      return po ? launch_replay_occ<NMV, 1, false, true, 0, kCtaWarps, false>(a, st, wpc, smem_per_warp)                \
+                : launch_replay_occ<NMV, 1, false, false, 0, kCtaWarps, false>(a, st, wpc, smem_per_warp);              \
     }                                                                                                             \
     if constexpr (NMV == 5) /* traced: run() / Simulation.run() of the overload geometry */                     \
       if (minb == 0 && po && overload_geometry(a) && a.models.stride == 8)                                       \
