@@ -696,8 +696,11 @@ def run_reference(args):
                                    f"{threads} threads (OpenMP)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "same_steps": True, "native_so_loaded": libs,
-        "reference_note": "the reference (pkg/src/infersim) is pure Python and cannot run on the GPU box; "
-                          "its CPU path is timed as the plain-C port that reproduces it bit for bit",
+        "reference_note": "the reference (pkg/src/infersim) is pure Python with no compiled path for oracle/_ref, "
+                          "so its CPU path is timed as the plain-C port that reproduces it bit for bit; the "
+                          "Python reference itself (baseline/_ref) is timed per propose in "
+                          "profiles/r02_propose_latency.json and bound through our engine in "
+                          "profiles/r02_reference_binding.json",
     }
     assert all(p.startswith("oracle/") for p in libs), f"reference arm mapped product code: {libs}"
     print(json.dumps(line), flush=True)
